@@ -1,0 +1,117 @@
+/*
+ * mrfp4.h -- C ABI of libmrfp4.so, the B200 (sm_100a) MR-GPTQ FP4 quantized-linear path.
+ *
+ * The reference (microfp 0.1.0, /root/reference/pkg/src/microfp) exposes this hot path
+ * as a Python API, not an FFI.  Each entry point below replaces one reference call
+ * (paths relative to /root/reference):
+ *
+ *   mrfp4_act_quant     quantize_rtn(X, FormatSpec.mxfp4()|nvfp4(), transform=TransformSpec.hadamard(k))
+ *                       pkg/src/microfp/quantizers.py:247-255 (with transforms.py:77-91,
+ *                       quantizers.py:170-215, formats.py:94-113/220-251/393-416)
+ *   mrfp4_sf_swizzle    MfpTensor.scale_codes (row-major, formats.py:314-316, :327) ->
+ *                       tensor-core scale layout; used by weight prep (MfpTensor -> device)
+ *   mrfp4_sf_unswizzle  inverse, to hand results back as a reference MfpTensor
+ *   mrfp4_gemm          dequantize(Aq) @ dequantize(Wq).T  (formats.py:424-442)
+ *   mrfp4_dequantize    dequantize(t) (formats.py:424-442) on the device, for checks
+ *
+ * Conventions
+ *   - All buffers are device pointers allocated by the caller; the library never
+ *     allocates on the hot path.  `stream` is a cudaStream_t (NULL = legacy default).
+ *   - Calls are stream-ordered and thread-safe.  Host-side argument checks return
+ *     a status synchronously; data errors found on the device (non-finite input,
+ *     NVFP4 E4M3 scale underflow -- both DataError in the reference,
+ *     quantizers.py:99-100, formats.py:101-102) are OR-ed into the caller's
+ *     device `status` word as MRFP4_STATUS_* bits.
+ *   - mrfp4_last_error() returns a thread-local message for the last failing call.
+ *
+ * Layouts
+ *   codes : uint8 [rows, K/2], row-major, element 2j in the low nibble of byte j
+ *           (identical to MfpTensor.codes, formats.py:377-382).
+ *   sf    : uint8, swizzled 128x4-atom layout, size mrfp4_sf_bytes(rows, K/G);
+ *           offset(r,c) = ((r/128)*ceil(C/4) + c/4)*512 + (r%32)*16 + ((r/32)%4)*4 + c%4,
+ *           padding rows/columns are zero.
+ *   MXFP4 : G = 32, E8M0 scale codes, tensor scale f32(4/3)      (formats.py:302-303)
+ *   NVFP4 : G = 16, E4M3 scale codes, whole-tensor global scale   (formats.py:306-307)
+ */
+#ifndef MRFP4_H_
+#define MRFP4_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MRFP4_ABI_VERSION 1
+
+/* return codes */
+#define MRFP4_OK 0
+#define MRFP4_EINVAL 1         /* bad shape / argument      -> DataError  */
+#define MRFP4_EUNSUPPORTED 2   /* unsupported configuration -> DataError  */
+#define MRFP4_ECUDA 3          /* CUDA launch/runtime error -> RuntimeError */
+
+/* formats */
+#define MRFP4_FMT_MXFP4 0
+#define MRFP4_FMT_NVFP4 1
+
+/* element dtypes (inputs / outputs) */
+#define MRFP4_DT_BF16 0
+#define MRFP4_DT_F16 1
+#define MRFP4_DT_F32 2
+
+/* device status bits */
+#define MRFP4_STATUS_NONFINITE 1u        /* NaN/Inf in the input (quantizers.py:99-100) */
+#define MRFP4_STATUS_SCALE_UNDERFLOW 2u  /* NVFP4 group scale code 0 -> eff = 0 (formats.py:101-102) */
+
+int mrfp4_abi_version(void);
+const char* mrfp4_last_error(void);
+
+/* Group size of a format (32 or 16), or 0 for an unknown format. */
+int mrfp4_group_size(int fmt);
+
+/* Bytes of a swizzled scale-factor buffer for a [rows, sf_cols] scale matrix. */
+size_t mrfp4_sf_bytes(int64_t rows, int64_t sf_cols);
+
+/* Device workspace needed by mrfp4_act_quant (NVFP4 needs 4 bytes for the tensor max). */
+size_t mrfp4_act_quant_workspace(int64_t M, int64_t K, int fmt);
+
+/*
+ * Fused online activation quantization (K1): y = X (.) blockdiag(H_k/sqrt(k)) ->
+ * group absmax -> scale codes written straight into the swizzled layout ->
+ * E2M1 codes, 2 per byte.  had_k in {0 (no rotation), 16, 32, 64, 128}.
+ * x: [M, K] with row stride ldx elements (ldx*elt_size % 16 == 0), dtype x_dtype.
+ * tensor_scale: device float, receives f32(4/3) (MXFP4) or the NVFP4 global scale.
+ * NVFP4 runs two stream-ordered passes (whole-tensor max, then encode).
+ */
+int mrfp4_act_quant(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ldx,
+                    int fmt, int had_k,
+                    uint8_t* codes, uint8_t* sf, float* tensor_scale,
+                    uint32_t* status, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Row-major [rows, sf_cols] scale codes <-> swizzled layout (padding written as 0). */
+int mrfp4_sf_swizzle(const uint8_t* sf_rowmajor, uint8_t* sf_swizzled,
+                     int64_t rows, int64_t sf_cols, void* stream);
+int mrfp4_sf_unswizzle(const uint8_t* sf_swizzled, uint8_t* sf_rowmajor,
+                       int64_t rows, int64_t sf_cols, void* stream);
+
+/*
+ * Block-scaled FP4 x FP4 GEMM (K2) on tcgen05.mma kind::mxf4nvf4:
+ *   D[M,N] = a_ts * b_ts * sum_k (sfA * a) (sfB * b)      (both operands K-major)
+ * a: [M, K/2] codes + swizzled sf; b: [N, K/2] codes + swizzled sf (the weight);
+ * a_ts, b_ts: device float tensor scales; d: [M, N] row stride ldd, dtype d_dtype
+ * (MRFP4_DT_BF16 or MRFP4_DT_F32).  Requires K % 64 == 0, N % 8 == 0.
+ */
+int mrfp4_gemm(const uint8_t* a, const uint8_t* a_sf, const float* a_ts,
+               const uint8_t* b, const uint8_t* b_sf, const float* b_ts,
+               void* d, int d_dtype, int64_t M, int64_t N, int64_t K, int64_t ldd,
+               int fmt, void* stream);
+
+/* Device dequantize (formats.py:424-442): out[r,c] = ts * scale * fp4, fp32 output. */
+int mrfp4_dequantize(const uint8_t* codes, const uint8_t* sf, const float* tensor_scale,
+                     int64_t rows, int64_t cols, int fmt, float* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MRFP4_H_ */

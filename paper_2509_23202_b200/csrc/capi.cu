@@ -1,0 +1,133 @@
+// extern "C" boundary of libmrfp4.so (declared in include/mrfp4.h).
+// Host-side validation mirrors the reference's DataError conditions
+// (/root/reference/pkg/src/microfp/quantizers.py:95-111) and returns a status;
+// kernels report data errors through the caller's device status word.
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+
+#include "common.cuh"
+
+namespace mrfp4 {
+int launch_act_quant(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ldx, int fmt, int hk, uint8_t* codes,
+                     uint8_t* sf, float* tensor_scale, uint32_t* status, void* workspace, cudaStream_t s);
+int launch_gemm_fp4(const uint8_t* a, const uint8_t* a_sf, const float* a_ts, const uint8_t* b, const uint8_t* b_sf,
+                    const float* b_ts, void* d, int d_dtype, int64_t M, int64_t N, int64_t K, int64_t ldd, int fmt,
+                    cudaStream_t s);
+int launch_sf_swizzle(const uint8_t* src, uint8_t* dst, int64_t rows, int64_t cols, cudaStream_t s);
+int launch_sf_unswizzle(const uint8_t* src, uint8_t* dst, int64_t rows, int64_t cols, cudaStream_t s);
+int launch_dequantize(const uint8_t* codes, const uint8_t* sf, const float* ts, int64_t rows, int64_t cols, int fmt,
+                      float* out, cudaStream_t s);
+}  // namespace mrfp4
+
+namespace {
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int cuda_status(int rc, const char* what) {
+  if (rc == MRFP4_OK) return MRFP4_OK;
+  if (rc == MRFP4_ECUDA) {
+    cudaError_t e = cudaGetLastError();
+    return fail(rc, "%s: CUDA error %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+  }
+  return fail(rc, "%s: unsupported configuration", what);
+}
+
+bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+int elt_size(int dt) { return dt == MRFP4_DT_F32 ? 4 : (dt == MRFP4_DT_BF16 || dt == MRFP4_DT_F16) ? 2 : 0; }
+}  // namespace
+
+extern "C" {
+
+int mrfp4_abi_version(void) { return MRFP4_ABI_VERSION; }
+
+const char* mrfp4_last_error(void) { return g_err.c_str(); }
+
+int mrfp4_group_size(int fmt) { return fmt == MRFP4_FMT_MXFP4 ? 32 : fmt == MRFP4_FMT_NVFP4 ? 16 : 0; }
+
+size_t mrfp4_sf_bytes(int64_t rows, int64_t sf_cols) {
+  if (rows <= 0 || sf_cols <= 0) return 0;
+  return (size_t)(mrfp4::ceil_div(rows, 128) * 128 * mrfp4::ceil_div(sf_cols, 4) * 4);
+}
+
+size_t mrfp4_act_quant_workspace(int64_t, int64_t, int fmt) { return fmt == MRFP4_FMT_NVFP4 ? 16 : 0; }
+
+int mrfp4_act_quant(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ldx, int fmt, int had_k, uint8_t* codes,
+                    uint8_t* sf, float* tensor_scale, uint32_t* status, void* workspace, size_t workspace_bytes,
+                    void* stream) {
+  const int G = mrfp4_group_size(fmt);
+  if (G == 0) return fail(MRFP4_EUNSUPPORTED, "unknown format %d", fmt);
+  const int es = elt_size(x_dtype);
+  if (es == 0) return fail(MRFP4_EUNSUPPORTED, "unsupported input dtype %d", x_dtype);
+  if (M < 1 || K < 1) return fail(MRFP4_EINVAL, "expected a non-empty 2-D matrix");  // quantizers.py:97-98
+  if (K % G) return fail(MRFP4_EINVAL, "columns (%lld) not divisible by group size (%d)", (long long)K, G);
+  if (had_k != 0 && had_k != 16 && had_k != 32 && had_k != 64 && had_k != 128)
+    return fail(MRFP4_EUNSUPPORTED, "unsupported Hadamard block %d (GPU path: 16, 32, 64, 128)", had_k);
+  if (had_k && K % had_k)
+    return fail(MRFP4_EINVAL, "columns (%lld) not divisible by transform block (%d)", (long long)K, had_k);
+  if (ldx < K) return fail(MRFP4_EINVAL, "row stride %lld < columns %lld", (long long)ldx, (long long)K);
+  if (!x || !codes || !sf || !tensor_scale) return fail(MRFP4_EINVAL, "null buffer");
+  if (((uint64_t)ldx * es) % 16 || !aligned(x, 16))
+    return fail(MRFP4_EUNSUPPORTED, "input rows must be 16-byte aligned");
+  if (!aligned(codes, 16) || !aligned(sf, 2)) return fail(MRFP4_EUNSUPPORTED, "output buffers must be 16-byte aligned");
+  if (fmt == MRFP4_FMT_NVFP4 && (workspace == nullptr || workspace_bytes < 4))
+    return fail(MRFP4_EINVAL, "NVFP4 needs a >= 4-byte device workspace");
+  const int rc = mrfp4::launch_act_quant(x, x_dtype, M, K, ldx, fmt, had_k, codes, sf, tensor_scale, status,
+                                         workspace, static_cast<cudaStream_t>(stream));
+  return cuda_status(rc, "mrfp4_act_quant");
+}
+
+int mrfp4_sf_swizzle(const uint8_t* src, uint8_t* dst, int64_t rows, int64_t cols, void* stream) {
+  if (rows < 1 || cols < 1 || !src || !dst) return fail(MRFP4_EINVAL, "bad scale matrix");
+  return cuda_status(mrfp4::launch_sf_swizzle(src, dst, rows, cols, static_cast<cudaStream_t>(stream)),
+                     "mrfp4_sf_swizzle");
+}
+
+int mrfp4_sf_unswizzle(const uint8_t* src, uint8_t* dst, int64_t rows, int64_t cols, void* stream) {
+  if (rows < 1 || cols < 1 || !src || !dst) return fail(MRFP4_EINVAL, "bad scale matrix");
+  return cuda_status(mrfp4::launch_sf_unswizzle(src, dst, rows, cols, static_cast<cudaStream_t>(stream)),
+                     "mrfp4_sf_unswizzle");
+}
+
+int mrfp4_gemm(const uint8_t* a, const uint8_t* a_sf, const float* a_ts, const uint8_t* b, const uint8_t* b_sf,
+               const float* b_ts, void* d, int d_dtype, int64_t M, int64_t N, int64_t K, int64_t ldd, int fmt,
+               void* stream) {
+  if (mrfp4_group_size(fmt) == 0) return fail(MRFP4_EUNSUPPORTED, "unknown format %d", fmt);
+  if (d_dtype != MRFP4_DT_BF16 && d_dtype != MRFP4_DT_F32)
+    return fail(MRFP4_EUNSUPPORTED, "output dtype must be bf16 or f32");
+  if (M < 1 || N < 1 || K < 1) return fail(MRFP4_EINVAL, "empty GEMM");
+  if (K % 64) return fail(MRFP4_EUNSUPPORTED, "K (%lld) must be a multiple of 64", (long long)K);
+  if (N % 8) return fail(MRFP4_EUNSUPPORTED, "N (%lld) must be a multiple of 8", (long long)N);
+  if (ldd < N) return fail(MRFP4_EINVAL, "ldd < N");
+  if (!a || !a_sf || !a_ts || !b || !b_sf || !b_ts || !d) return fail(MRFP4_EINVAL, "null buffer");
+  if (!aligned(a, 16) || !aligned(b, 16) || !aligned(a_sf, 16) || !aligned(b_sf, 16) || !aligned(d, 16) ||
+      (ldd * elt_size(d_dtype)) % 16)
+    return fail(MRFP4_EUNSUPPORTED, "GEMM buffers must be 16-byte aligned");
+  const int rc = mrfp4::launch_gemm_fp4(a, a_sf, a_ts, b, b_sf, b_ts, d, d_dtype, M, N, K, ldd, fmt,
+                                        static_cast<cudaStream_t>(stream));
+  return cuda_status(rc, "mrfp4_gemm");
+}
+
+int mrfp4_dequantize(const uint8_t* codes, const uint8_t* sf, const float* tensor_scale, int64_t rows, int64_t cols,
+                     int fmt, float* out, void* stream) {
+  const int G = mrfp4_group_size(fmt);
+  if (G == 0) return fail(MRFP4_EUNSUPPORTED, "unknown format %d", fmt);
+  if (rows < 1 || cols < 1 || cols % G || cols % 2) return fail(MRFP4_EINVAL, "bad dimensions");
+  if (!codes || !sf || !tensor_scale || !out) return fail(MRFP4_EINVAL, "null buffer");
+  return cuda_status(mrfp4::launch_dequantize(codes, sf, tensor_scale, rows, cols, fmt, out,
+                                              static_cast<cudaStream_t>(stream)),
+                     "mrfp4_dequantize");
+}
+
+}  // extern "C"

@@ -1,0 +1,321 @@
+// K2: block-scaled FP4 x FP4 GEMM on the 5th-gen tensor cores (sm_100a).
+//
+// Computes the quantized linear Q(X H) Q(W H)^T of PAPER.md:337 -- in the
+// reference only defined by composition, dequantize(Aq) @ dequantize(Wq).T
+// (/root/reference/pkg/src/microfp/formats.py:424-442):
+//     D[m, n] = ts_A * ts_W * sum_k (sfA[m, k/G] * a[m, k]) * (sfB[n, k/G] * w[n, k])
+//
+// Structure (one CTA per SM, persistent over 128 x BN output tiles):
+//   warp 0      TMA producer: A/B code tiles via cp.async.bulk.tensor (128-B swizzle),
+//               scale-factor atoms via cp.async.bulk, into a kStages-deep mbarrier ring
+//   warp 1      TMEM allocator + single-thread MMA issuer: tcgen05.cp moves the
+//               stage's scale factors SMEM -> TMEM, then tcgen05.mma
+//               kind::mxf4nvf4.block_scale (scale_vec::4X ue4m3 for NVFP4,
+//               ::2X ue8m0 for MXFP4) accumulates in TMEM; tcgen05.commit frees
+//               the stage
+//   warps 2-5   epilogue: tcgen05.ld 32 columns at a time, * ts_A*ts_W, -> bf16/f32
+//               global stores
+// Scale factors occupy a per-stage TMEM region so a stage's SF are only
+// overwritten after the MMAs that read them committed (same ring as SMEM).
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <mutex>
+
+#include "common.cuh"
+#include "sm100.cuh"
+
+namespace mrfp4 {
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 256;         // FP4 elements per k-block
+constexpr int BK_BYTES = BK / 2;
+constexpr int UMMA_K = 64;      // FP4 elements per tcgen05.mma
+constexpr int kThreads = 192;
+
+template <int VEC, int BN>
+struct Cfg {
+  static constexpr int kAtomsPerKb = BK / VEC / 4;  // 128x4 SF atoms per k-block: 4 (NVFP4) / 2 (MXFP4)
+  static constexpr int kNB = BN / 128;              // 128-row SF blocks of B per tile
+  static constexpr int kStages = 4;
+  static constexpr int kABytes = BM * BK_BYTES;
+  static constexpr int kBBytes = BN * BK_BYTES;
+  static constexpr int kSfaBytes = kAtomsPerKb * 512;
+  static constexpr int kSfbBytes = kNB * kAtomsPerKb * 512;
+  static constexpr int kSfaCols = kAtomsPerKb * 4;
+  static constexpr int kSfbCols = kNB * kAtomsPerKb * 4;
+  static constexpr int kAccCols = BN;
+  static constexpr int kTmemCols = 512;
+  static_assert(kAccCols + kStages * (kSfaCols + kSfbCols) <= kTmemCols, "TMEM budget");
+  static constexpr int kOffA = 0;
+  static constexpr int kOffB = kOffA + kStages * kABytes;
+  static constexpr int kOffSfa = kOffB + kStages * kBBytes;
+  static constexpr int kOffSfb = kOffSfa + kStages * kSfaBytes;
+  static constexpr int kOffBar = kOffSfb + kStages * kSfbBytes;
+  static constexpr int kSmem = kOffBar + 256 + 1024;  // barriers + 1024-B alignment slack
+};
+
+__host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+
+struct GemmArgs {
+  const uint8_t* a_sf;
+  const uint8_t* b_sf;
+  const float* a_ts;
+  const float* b_ts;
+  void* d;
+  int64_t M, N, K, ldd;
+  int64_t sf_col_blocks;  // ceil(K / VEC / 4)
+  int64_t b_row_blocks;   // ceil(N / 128)
+  int num_m_blk, num_n_blk, num_kb;
+};
+
+template <int VEC, int BN, int OUT>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_gemm_fp4(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs g) {
+  using C = Cfg<VEC, BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
+  uint64_t* empty = full + C::kStages;
+  uint64_t* tfull = empty + C::kStages;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    sm100::tma_prefetch_desc(&tmA);
+    sm100::tma_prefetch_desc(&tmB);
+    for (int s = 0; s < C::kStages; ++s) {
+      sm100::mbar_init(&full[s], 1);
+      sm100::mbar_init(&empty[s], 1);
+    }
+    sm100::mbar_init(tfull, 1);
+    sm100::mbar_init(tempty, 4);
+    sm100::fence_mbar_init();
+  }
+  if (warp == 1) sm100::tmem_alloc(tmem_holder, C::kTmemCols);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  const int num_tiles = g.num_m_blk * g.num_n_blk;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int m_blk = tile % g.num_m_blk, n_blk = tile / g.num_m_blk;
+        for (int kb = 0; kb < g.num_kb; ++kb) {
+          sm100::mbar_wait(&empty[stage], phase ^ 1);
+          const int atoms = (int)imin64(C::kAtomsPerKb, g.sf_col_blocks - (int64_t)kb * C::kAtomsPerKb);
+          int nbv = 0;
+#pragma unroll
+          for (int j = 0; j < C::kNB; ++j) nbv += ((int64_t)n_blk * C::kNB + j < g.b_row_blocks);
+          const uint32_t bytes = C::kABytes + C::kBBytes + (uint32_t)atoms * 512u * (1u + nbv);
+          sm100::mbar_arrive_expect_tx(&full[stage], bytes);
+          sm100::tma_load_2d(smem + C::kOffA + stage * C::kABytes, &tmA, &full[stage], kb * BK_BYTES, m_blk * BM);
+          sm100::tma_load_2d(smem + C::kOffB + stage * C::kBBytes, &tmB, &full[stage], kb * BK_BYTES, n_blk * BN);
+          const int64_t katom = (int64_t)kb * C::kAtomsPerKb;
+          sm100::bulk_load(smem + C::kOffSfa + stage * C::kSfaBytes,
+                           g.a_sf + ((int64_t)m_blk * g.sf_col_blocks + katom) * 512, atoms * 512u, &full[stage]);
+#pragma unroll
+          for (int j = 0; j < C::kNB; ++j) {
+            const int64_t rb = (int64_t)n_blk * C::kNB + j;
+            if (rb < g.b_row_blocks)
+              sm100::bulk_load(smem + C::kOffSfb + stage * C::kSfbBytes + j * C::kAtomsPerKb * 512,
+                               g.b_sf + (rb * g.sf_col_blocks + katom) * 512, atoms * 512u, &full[stage]);
+          }
+          if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0, acc_phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        sm100::mbar_wait(tempty, acc_phase ^ 1);
+        sm100::tc_fence_after();
+        for (int kb = 0; kb < g.num_kb; ++kb) {
+          sm100::mbar_wait(&full[stage], phase);
+          sm100::tc_fence_after();
+          const int atoms = (int)imin64(C::kAtomsPerKb, g.sf_col_blocks - (int64_t)kb * C::kAtomsPerKb);
+          const uint32_t sfa_t = tmem_base + C::kAccCols + stage * (C::kSfaCols + C::kSfbCols);
+          const uint32_t sfb_t = sfa_t + C::kSfaCols;
+          const uint32_t sfa_s = sm100::smem_u32(smem + C::kOffSfa + stage * C::kSfaBytes);
+          const uint32_t sfb_s = sm100::smem_u32(smem + C::kOffSfb + stage * C::kSfbBytes);
+          for (int a = 0; a < atoms; ++a) {
+            sm100::tc_cp_32x128b_warpx4(sfa_t + a * 4, sm100::smem_desc(sfa_s + a * 512, 0, 128, 0));
+#pragma unroll
+            for (int j = 0; j < C::kNB; ++j)
+              sm100::tc_cp_32x128b_warpx4(sfb_t + a * C::kNB * 4 + j * 4,
+                                          sm100::smem_desc(sfb_s + (j * C::kAtomsPerKb + a) * 512, 0, 128, 0));
+          }
+          const uint32_t a_s = sm100::smem_u32(smem + C::kOffA + stage * C::kABytes);
+          const uint32_t b_s = sm100::smem_u32(smem + C::kOffB + stage * C::kBBytes);
+          const int nk = (int)imin64(BK / UMMA_K, (g.K - (int64_t)kb * BK) / UMMA_K);
+          for (int k = 0; k < nk; ++k) {
+            const int atom = VEC == 16 ? k : (k >> 1);
+            const uint32_t sfid = VEC == 16 ? 0u : (uint32_t)(k & 1) * 2u;
+            const uint64_t adesc = sm100::smem_desc(a_s + k * (UMMA_K / 2), 16, 1024, 2);
+            const uint64_t bdesc = sm100::smem_desc(b_s + k * (UMMA_K / 2), 16, 1024, 2);
+            const uint32_t idesc = sm100::idesc_fp4(BM, BN, VEC == 32, sfid, sfid);
+            sm100::tc_mma_fp4<VEC>(tmem_base, adesc, bdesc, idesc, (sfa_t + atom * 4) | (sfid << 30),
+                                   (sfb_t + atom * C::kNB * 4) | (sfid << 30), (kb | k) != 0);
+          }
+          sm100::tc_commit(&empty[stage]);
+          if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+        }
+        sm100::tc_commit(tfull);
+        acc_phase ^= 1;
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    const float alpha = __ldg(g.a_ts) * __ldg(g.b_ts);
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      const int m_blk = tile % g.num_m_blk, n_blk = tile / g.num_m_blk;
+      sm100::mbar_wait(tfull, acc_phase);
+      sm100::tc_fence_after();
+      const int64_t row = (int64_t)m_blk * BM + q * 32 + lane;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t r[32];
+        sm100::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + c, r);
+        sm100::tmem_ld_wait();
+        const int64_t col = (int64_t)n_blk * BN + c;
+        if (row < g.M) {
+          if constexpr (OUT == MRFP4_DT_BF16) {
+            __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(g.d) + row * g.ldd + col;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              if (col + 8 * j < g.N) {
+                uint32_t w[4];
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                  __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(r[8 * j + 2 * t]) * alpha,
+                                                           __uint_as_float(r[8 * j + 2 * t + 1]) * alpha);
+                  w[t] = *reinterpret_cast<uint32_t*>(&h);
+                }
+                *reinterpret_cast<uint4*>(dst + 8 * j) = make_uint4(w[0], w[1], w[2], w[3]);
+              }
+            }
+          } else {
+            float* dst = static_cast<float*>(g.d) + row * g.ldd + col;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              if (col + 4 * j < g.N) {
+                *reinterpret_cast<float4*>(dst + 4 * j) =
+                    make_float4(__uint_as_float(r[4 * j]) * alpha, __uint_as_float(r[4 * j + 1]) * alpha,
+                                __uint_as_float(r[4 * j + 2]) * alpha, __uint_as_float(r[4 * j + 3]) * alpha);
+              }
+            }
+          }
+        }
+      }
+      sm100::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive(tempty);
+      acc_phase ^= 1;
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc(tmem_base, C::kTmemCols);
+  }
+}
+
+// ---------------------------------------------------------------- host side
+PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+bool make_code_map(CUtensorMap* tm, const uint8_t* ptr, int64_t rows, int64_t K, int box_rows) {
+  auto encode = get_encode_fn();
+  if (!encode) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)(K / 2), (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(K / 2)};
+  cuuint32_t box[2] = {(cuuint32_t)BK_BYTES, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(ptr), dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <int VEC, int BN, int OUT>
+int launch(const uint8_t* a, const uint8_t* b, const GemmArgs& args0, cudaStream_t s) {
+  using C = Cfg<VEC, BN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(k_gemm_fp4<VEC, BN, OUT>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem) !=
+        cudaSuccess)
+      return MRFP4_ECUDA;
+    attr_set = true;
+  }
+  GemmArgs g = args0;
+  CUtensorMap tmA, tmB;
+  if (!make_code_map(&tmA, a, g.M, g.K, BM) || !make_code_map(&tmB, b, g.N, g.K, BN)) return MRFP4_ECUDA;
+  g.num_m_blk = (int)ceil_div(g.M, BM);
+  g.num_n_blk = (int)ceil_div(g.N, BN);
+  g.num_kb = (int)ceil_div(g.K, BK);
+  g.sf_col_blocks = ceil_div(g.K / VEC, 4);
+  g.b_row_blocks = ceil_div(g.N, 128);
+  const int tiles = g.num_m_blk * g.num_n_blk;
+  const int grid = std::min(tiles, num_sms());
+  k_gemm_fp4<VEC, BN, OUT><<<grid, kThreads, C::kSmem, s>>>(tmA, tmB, g);
+  return cudaPeekAtLastError() == cudaSuccess ? MRFP4_OK : MRFP4_ECUDA;
+}
+
+}  // namespace
+
+int launch_gemm_fp4(const uint8_t* a, const uint8_t* a_sf, const float* a_ts, const uint8_t* b, const uint8_t* b_sf,
+                    const float* b_ts, void* d, int d_dtype, int64_t M, int64_t N, int64_t K, int64_t ldd, int fmt,
+                    cudaStream_t s) {
+  GemmArgs g{};
+  g.a_sf = a_sf;
+  g.b_sf = b_sf;
+  g.a_ts = a_ts;
+  g.b_ts = b_ts;
+  g.d = d;
+  g.M = M;
+  g.N = N;
+  g.K = K;
+  g.ldd = ldd;
+  if (fmt == MRFP4_FMT_NVFP4) {
+    return d_dtype == MRFP4_DT_BF16 ? launch<16, 256, MRFP4_DT_BF16>(a, b, g, s)
+                                    : launch<16, 256, MRFP4_DT_F32>(a, b, g, s);
+  }
+  return d_dtype == MRFP4_DT_BF16 ? launch<32, 256, MRFP4_DT_BF16>(a, b, g, s)
+                                  : launch<32, 256, MRFP4_DT_F32>(a, b, g, s);
+}
+
+}  // namespace mrfp4

@@ -1,0 +1,159 @@
+"""Weight preparation (K3) and the quantized linear (K1 + K2).
+
+The reference has no linear function: the paper's layer is
+``Q(X H_k) Q(W H_k)^T``, i.e. ``dequantize(Aq) @ dequantize(Wq).T``
+with ``Aq = quantize_rtn(X, spec, transform=H_k)`` online and ``Wq`` from
+``quantize_rtn(W, ..., H_k)`` / ``mr_gptq`` offline
+(/root/reference/pkg/src/microfp/formats.py:424-442, quantizers.py:247-255,
+gptq.py:274-300).  Here:
+
+* ``prepare_weight`` validates a reference ``MfpTensor`` (or ``QuantResult``) and
+  uploads its codes unchanged (same nibble order) and its scale codes swizzled into
+  the tensor-core layout (``mrfp4_sf_swizzle``).  Fitted E8M0 grids
+  (``scale_fit``, quantizers.py:144-154) have no hardware encoding and are rejected.
+* ``quantize_weight`` is the GPU RTN of a dense weight (bit-identical to
+  ``quantize_rtn(W, spec, transform=H_k)``, transforms.py:94-100 rotation folded).
+* ``quantized_linear`` runs K1 on the activations and K2 (tcgen05 block-scaled GEMM).
+"""
+
+from __future__ import annotations
+
+import dataclasses
+import os
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import DataError
+from .formats import GROUP, format_code, spec_for
+from .quantize import GpuQuantResult, act_quant_into, alloc_result, as_device_matrix, quantize_rtn
+from .transforms import hadamard_block, transform_for
+
+_OUT = {torch.bfloat16: _lib.DT_BF16, torch.float32: _lib.DT_F32}
+
+
+@dataclasses.dataclass
+class PackedWeight:
+    """A weight [N, K] in the GEMM's device layout."""
+
+    fmt: int
+    had_k: int
+    N: int
+    K: int
+    codes: torch.Tensor             # uint8 [N, K/2]
+    sf: torch.Tensor                # uint8 swizzled scales
+    tensor_scale_dev: torch.Tensor  # float32 [1]
+
+    @property
+    def spec(self):
+        return spec_for(self.fmt)
+
+    @property
+    def transform(self):
+        return transform_for(self.had_k)
+
+    @property
+    def device(self):
+        return self.codes.device
+
+    def shard(self, rank: int, world: int) -> "PackedWeight":
+        """Rows [rank*N/P, (rank+1)*N/P) of the weight (column-parallel linear)."""
+        if self.N % (world * 128):
+            raise DataError(f"N={self.N} must split into multiples of 128 rows across {world} ranks")
+        n = self.N // world
+        r0 = rank * n
+        G = GROUP[self.fmt]
+        cb = -(-(self.K // G) // 4)
+        atoms = slice((r0 // 128) * cb * 512, ((r0 + n) // 128) * cb * 512)  # 128-row SF blocks are contiguous
+        return PackedWeight(self.fmt, self.had_k, n, self.K, self.codes[r0:r0 + n].contiguous(),
+                            self.sf[atoms].contiguous(), self.tensor_scale_dev.clone())
+
+
+def _validate_gemm_k(K: int) -> None:
+    if K % 64:
+        raise DataError(f"unsupported on GPU path: K={K} must be a multiple of 64 for the FP4 GEMM")
+
+
+def prepare_weight(w, device=None) -> PackedWeight:
+    """MfpTensor / QuantResult / GpuQuantResult / MFPQ path -> PackedWeight on the GPU."""
+    if isinstance(w, PackedWeight):
+        return w
+    if isinstance(w, GpuQuantResult):
+        _validate_gemm_k(w.cols)
+        return PackedWeight(w.fmt, w.had_k, w.rows, w.cols, w.codes, w.sf, w.tensor_scale_dev)
+    if isinstance(w, (str, os.PathLike)):
+        from .fileio import read_quant
+        w, _perm = read_quant(w)  # the permutation section is informational (codes are un-permuted)
+    if hasattr(w, "tensor") and not hasattr(w, "codes"):
+        w = w.tensor  # reference QuantResult
+    for attr in ("spec", "rows", "cols", "codes", "scale_codes", "tensor_scale"):
+        if not hasattr(w, attr):
+            raise DataError(f"prepare_weight: expected an MfpTensor-like object (missing {attr!r})")
+    fmt = format_code(w.spec)
+    if getattr(w, "scale_fit", None) is not None:
+        raise DataError("unsupported on GPU path: scale_fit weights (fitted E8M0 grid 2^(a*q+b) is not "
+                        "hardware E8M0; re-quantize with absmax scales, cli.py --scale-opt absmax)")
+    had_k = hadamard_block(getattr(w, "transform", None))
+    N, K = int(w.rows), int(w.cols)
+    G = GROUP[fmt]
+    _validate_gemm_k(K)
+    codes = np.ascontiguousarray(np.asarray(w.codes, dtype=np.uint8).reshape(N, K // 2))
+    sc = np.asarray(w.scale_codes)
+    if sc.dtype.kind == "f":
+        raise DataError("unsupported on GPU path: unquantized (float) scales")
+    sc = np.ascontiguousarray(sc.astype(np.uint8).reshape(N, K // G))
+    if fmt == 1 and sc.size and sc.max() > 126:
+        raise DataError("reserved scale code in container")
+    ts = float(w.tensor_scale)
+    if not np.isfinite(ts) or ts <= 0:
+        raise DataError("tensor_scale must be finite and positive")
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2509_23202_b200 needs a CUDA device (sm_100a); there is no CPU path")
+    dev = torch.device(device or "cuda")
+    d_codes = torch.from_numpy(codes).to(dev)
+    d_sc = torch.from_numpy(sc).to(dev)
+    d_sf = torch.empty(_lib.lib().mrfp4_sf_bytes(N, K // G), dtype=torch.uint8, device=dev)
+    _lib.check(_lib.lib().mrfp4_sf_swizzle(_lib.ptr(d_sc), _lib.ptr(d_sf), N, K // G,
+                                           _lib.stream_ptr(torch, dev)))
+    d_ts = torch.tensor([ts], dtype=torch.float32, device=dev)
+    return PackedWeight(fmt, had_k, N, K, d_codes, d_sf, d_ts)
+
+
+def quantize_weight(W, spec, transform=None, *, check: bool = True) -> PackedWeight:
+    """GPU RTN of a dense weight with the rotation folded in (transforms.py:94-100)."""
+    return prepare_weight(quantize_rtn(W, spec, transform=transform, check=check))
+
+
+def gemm(a: GpuQuantResult, w: PackedWeight, out: torch.Tensor) -> torch.Tensor:
+    """K2 only: out[M, N] = a . w^T with both operands already quantized."""
+    if a.fmt != w.fmt or a.cols != w.K:
+        raise DataError("activation / weight format or K mismatch")
+    _lib.check(_lib.lib().mrfp4_gemm(
+        _lib.ptr(a.codes), _lib.ptr(a.sf), _lib.ptr(a.tensor_scale_dev),
+        _lib.ptr(w.codes), _lib.ptr(w.sf), _lib.ptr(w.tensor_scale_dev),
+        _lib.ptr(out), _OUT[out.dtype], a.rows, w.N, w.K, out.stride(0), w.fmt,
+        _lib.stream_ptr(torch, out.device)))
+    return out
+
+
+def quantized_linear(x, w: PackedWeight, *, out_dtype=torch.bfloat16, out: torch.Tensor | None = None,
+                     check: bool = False) -> torch.Tensor:
+    """y = Q(x H_k) Q(W H_k)^T for x [..., K] (bf16/fp16/fp32), W prepared by prepare_weight."""
+    if not isinstance(w, PackedWeight):
+        w = prepare_weight(w)
+    if out_dtype not in _OUT:
+        raise DataError("out_dtype must be torch.bfloat16 or torch.float32")
+    lead = tuple(x.shape[:-1]) if isinstance(x, torch.Tensor) else None
+    x2 = as_device_matrix(x.reshape(-1, x.shape[-1]) if isinstance(x, torch.Tensor) else x, w.device)
+    M, K = x2.shape
+    if K != w.K:
+        raise DataError(f"activation K={K} does not match weight K={w.K}")
+    a = alloc_result(M, K, w.fmt, w.had_k, x2.device)
+    act_quant_into(x2, w.fmt, w.had_k, a.codes, a.sf, a.tensor_scale_dev, a.scratch)
+    if check:
+        a.check()
+    if out is None:
+        out = torch.empty((M, w.N), dtype=out_dtype, device=x2.device)
+    gemm(a, w, out)
+    return out.reshape(*lead, w.N) if lead is not None and len(lead) != 1 else out

@@ -1,0 +1,136 @@
+"""K2 parity: tcgen05 block-scaled FP4 GEMM vs the oracle's dequantize-matmul.
+
+Oracle: ``dequantize(A) @ dequantize(W).T`` (formats.py:424-442) computed here in
+float64 from the same codes/scales.  Tolerance (north star): relative Frobenius
+error <= 1e-3; measured in fp32-output mode where only accumulation order differs
+(we assert <= 1e-5).  bf16 output is checked against bf16(Y_ref) to within one
+bf16 ulp per element (bf16 rounding alone is 1.66e-3 Frobenius).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import paper_2509_23202_b200 as P
+
+pytestmark = pytest.mark.gpu
+
+SPEC = {"mxfp4": P.FormatSpec.mxfp4(), "nvfp4": P.FormatSpec.nvfp4()}
+
+
+def random_container(rng, rows, cols, fmt, ts=None):
+    """Random valid codes/scales as an oracle-style quantization (no data needed)."""
+    G = 32 if fmt == "mxfp4" else 16
+    ec = rng.integers(0, 16, (rows, cols), dtype=np.uint8)
+    if fmt == "mxfp4":
+        sc = rng.integers(120, 135, (rows, cols // G), dtype=np.uint8)
+        ts = float(np.float32(4 / 3)) if ts is None else ts
+    else:
+        sc = rng.integers(1, 127, (rows, cols // G), dtype=np.uint8)
+        ts = float(np.float32(rng.uniform(0.001, 0.01))) if ts is None else ts
+    return O.OracleQuant(fmt, rows, cols, G, None, ec, sc, ts, 0.0, 0.0)
+
+
+def to_mfp(q):
+    return P.MfpTensor(SPEC[q.fmt], q.rows, q.cols, O.pack_nibbles(q.element_codes), q.scale_codes.reshape(-1),
+                       q.tensor_scale, None, None)
+
+
+def run_gemm(A, W, out_dtype=torch.float32):
+    a = P.prepare_weight(to_mfp(A))       # same device layout for activations
+    w = P.prepare_weight(to_mfp(W))
+    act = P.GpuQuantResult(a.fmt, a.N, a.K, 0, a.codes, a.sf, a.tensor_scale_dev,
+                           torch.zeros(8, dtype=torch.int32, device="cuda"))
+    out = torch.empty((A.rows, W.rows), dtype=out_dtype, device="cuda")
+    P.gemm(act, w, out)
+    torch.cuda.synchronize()
+    return out
+
+
+def ref64(A, W):
+    return O.dequantize(A) @ O.dequantize(W).T
+
+
+def rel_fro(y, ref):
+    return float(np.linalg.norm(y - ref) / max(np.linalg.norm(ref), 1e-300))
+
+
+@pytest.mark.parametrize("fmt", ["mxfp4", "nvfp4"])
+@pytest.mark.parametrize("M,N,K", [
+    (128, 256, 256), (1, 256, 64), (16, 512, 4096), (200, 384, 1024), (300, 264, 192), (512, 1024, 2048)])
+def test_gemm_random_codes_fp32(fmt, M, N, K):
+    rng = np.random.default_rng(M * 131 + N * 7 + K)
+    A, W = random_container(rng, M, K, fmt), random_container(rng, N, K, fmt)
+    y = run_gemm(A, W).cpu().numpy()
+    ref = ref64(A, W)
+    assert np.isfinite(y).all()
+    assert rel_fro(y, ref) <= 1e-5, rel_fro(y, ref)
+
+
+@pytest.mark.parametrize("fmt", ["mxfp4", "nvfp4"])
+def test_gemm_bf16_output_within_one_ulp(fmt):
+    rng = np.random.default_rng(5)
+    A, W = random_container(rng, 256, 1024, fmt), random_container(rng, 512, 1024, fmt)
+    y = run_gemm(A, W, torch.bfloat16).float().cpu().numpy()
+    ref = ref64(A, W)
+    refb = torch.from_numpy(ref.astype(np.float32)).bfloat16().float().numpy()
+    ulp = np.abs(refb) * 2.0 ** -7 + 1e-30
+    assert (np.abs(y - refb) <= ulp * 1.01).mean() >= 0.999
+    assert rel_fro(y, ref) <= 3e-3
+
+
+@pytest.mark.parametrize("fmt", ["mxfp4", "nvfp4"])
+def test_gemm_known_answer_single_group(fmt):
+    """One nonzero group per row: every code x every scale code passes through exactly."""
+    G = 32 if fmt == "mxfp4" else 16
+    K = 256
+    rng = np.random.default_rng(9)
+    A = random_container(rng, 128, K, fmt, ts=1.0)
+    W = random_container(rng, 256, K, fmt, ts=1.0)
+    A.element_codes[:] = 0
+    A.element_codes[:, :G] = np.arange(16, dtype=np.uint8)[np.arange(128 * G) % 16].reshape(128, G)
+    A.scale_codes[:, 0] = (np.arange(128) % 100 + (20 if fmt == "mxfp4" else 1)).astype(np.uint8)
+    y = run_gemm(A, W).cpu().numpy()
+    np.testing.assert_allclose(y, ref64(A, W), rtol=1e-6, atol=1e-30)
+
+
+@pytest.mark.parametrize("fmt", ["mxfp4", "nvfp4"])
+@pytest.mark.parametrize("k", [0, 16, 32, 128])
+def test_golden_linear(golden, fmt, k):
+    """End to end through quantized_linear on the reference's own linear fixtures."""
+    key = f"lin_{fmt}_k{k}"
+    A = torch.from_numpy(golden[key + "_a"]).cuda().bfloat16()
+    Wq = O.quantize_rtn(golden[key + "_w"], fmt, hadamard=k or None)
+    t = P.MfpTensor(SPEC[fmt], Wq.rows, Wq.cols, Wq.codes.reshape(-1), Wq.scale_codes.reshape(-1),
+                    Wq.tensor_scale, P.TransformSpec.hadamard(k) if k else None, None)
+    w = P.prepare_weight(t)
+    y = P.quantized_linear(A, w, out_dtype=torch.float32).cpu().numpy()
+    ref = golden[key + "_y"]
+    assert rel_fro(y, ref) <= 1e-5
+
+
+@pytest.mark.parametrize("fmt", ["mxfp4", "nvfp4"])
+def test_quantize_weight_matches_prepare_weight(fmt):
+    rng = np.random.default_rng(2)
+    W = O.bf16_round(rng.standard_normal((256, 512)) / 16)
+    X = O.bf16_round(rng.standard_normal((64, 512)))
+    tr = P.TransformSpec.hadamard(32)
+    w_gpu = P.quantize_weight(torch.from_numpy(W).cuda().bfloat16(), SPEC[fmt], tr)
+    Wq = O.quantize_rtn(W, fmt, hadamard=32)
+    Aq = O.quantize_rtn(X, fmt, hadamard=32)
+    y = P.quantized_linear(torch.from_numpy(X).cuda().bfloat16(), w_gpu, out_dtype=torch.float32)
+    ref = O.linear_reference(Aq, Wq)
+    assert rel_fro(y.cpu().numpy(), ref) <= 1e-4
+
+
+def test_weight_validation():
+    rng = np.random.default_rng(0)
+    q = random_container(rng, 128, 256, "mxfp4")
+    t = to_mfp(q)
+    bad = P.MfpTensor(t.spec, t.rows, t.cols, t.codes, t.scale_codes, t.tensor_scale, None, (0.1, -3.0))
+    with pytest.raises(P.DataError, match="scale_fit"):
+        P.prepare_weight(bad)
+    q2 = random_container(rng, 128, 96, "mxfp4")
+    with pytest.raises(P.DataError, match="multiple of 64"):
+        P.prepare_weight(to_mfp(q2))
