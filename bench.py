@@ -1,0 +1,343 @@
+#!/usr/bin/env python
+"""Benchmark of the MR-GPTQ FP4 quantized-linear hot path on B200 (driver contract).
+
+One *step* = one pass of the hot path over one batch: K1 (online Hadamard rotate +
+FP4 quantize of the activations, CUDA) then K2 (tcgen05 block-scaled FP4 GEMM
+against RTN weights prepared once).  Default workload = BASELINE.json configs[1]:
+Llama-3-8B MLP down_proj, K=14336 -> N=4096, 2048 tokens, MXFP4 + Hadamard-32.
+
+Reported (one JSON line from rank 0):
+  value / ms_per_step   FP4-linear TFLOP/s = 2*M*N*K / (t_K1 + t_K2), device time,
+                        inputs resident in HBM, L2 flushed (256 MiB memset) between steps
+  e2e                   same metric through the public API (quantized_linear) with the
+                        activations copied from pinned host memory and Y read back per step
+  roofline              dominant kernel (K2) vs 4x the measured bf16 peak; K1 vs measured HBM
+  cpu_baseline          the CPU oracle (numpy port of the reference) on a bounded sample
+  extras                cuBLAS-bf16 time of the same layer and the layer speedup over it,
+                        rot+quant GB/s, clocks sampled during the timed region
+--impl reference runs the CPU oracle (numpy restatement of microfp) on all host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (workload, M, K, N, fmt, hadamard)
+    "c1": ("llama3-8b mlp.down_proj 14336->4096, 2048 tokens, MXFP4+H32", 2048, 14336, 4096, "mxfp4", 32),
+    "c0": ("llama3-8b attn.q_proj 4096->4096, 16 tokens, NVFP4+H16", 16, 4096, 4096, "nvfp4", 16),
+    "c2-up-nv": ("llama3-70b mlp.up 8192->28672, 2048 tokens, NVFP4+H16", 2048, 8192, 28672, "nvfp4", 16),
+    "c2-down-mx": ("llama3-70b mlp.down 28672->8192, 2048 tokens, MXFP4+H32", 2048, 28672, 8192, "mxfp4", 32),
+    "c3-gateup": ("qwen3-32b mlp.gate_up 5120->51200, 2048 tokens, NVFP4+H128", 2048, 5120, 51200, "nvfp4", 128),
+    "c4": ("llama3-405b-shaped mlp 16384->53248, 8192 tokens, NVFP4+H16", 8192, 16384, 53248, "nvfp4", 16),
+}
+METRIC = "FP4 linear TFLOPS & speedup vs BF16 at Llama-3 shapes; rot+quant HBM GB/s"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), float(p["bf16_tflops"]), float(p.get("bf16_tflops_sustained", 0)), "measured"
+    except Exception:
+        return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region (B200_PROFILING.md)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.path = tempfile.mktemp(suffix=".csv")
+
+    def start(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "50",
+                 "-i", str(self.dev)], stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        self.proc.terminate()
+        self.proc.wait()
+        self.fh.close()
+        rows = []
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(rows[0][1]) if rows[0][1].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ----------------------------------------------------------------------------- CPU arms
+def cpu_linear_step(X, Wdeq, fmt, had, workers):
+    import oracle as O
+    q = O.quantize_rtn_parallel(X, fmt, had, workers=workers)
+    return O.dequantize_f32(q) @ Wdeq.T
+
+
+def cpu_inputs(M, K, N, fmt, had, seed=1234):
+    import numpy as np
+    import oracle as O
+    rng = np.random.default_rng(seed)
+    X = O.bf16_round(rng.standard_normal((M, K), dtype=np.float32))
+    W = O.bf16_round(rng.standard_normal((N, K), dtype=np.float32) / np.sqrt(K))
+    Wq = O.quantize_rtn_parallel(W, fmt, had)
+    return X, O.dequantize_f32(Wq)
+
+
+def run_reference(args, cfg, rank):
+    """--impl reference: the CPU oracle (numpy restatement of microfp) on all host cores."""
+    if rank != 0:
+        return
+    name, M, K, N, fmt, had = cfg
+    cores = len(os.sched_getaffinity(0))
+    X, Wdeq = cpu_inputs(M, K, N, fmt, had)
+    for _ in range(args.warmup):
+        cpu_linear_step(X, Wdeq, fmt, had, cores)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        cpu_linear_step(X, Wdeq, fmt, had, cores)
+    dt = (time.perf_counter() - t0) / args.steps
+    tflops = 2.0 * M * N * K / dt / 1e12
+    line = {
+        "impl": "reference", "metric": METRIC, "value": tflops, "unit": "TFLOP/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (bf16 N(0,1) acts, N(0,1/K) weights)",
+        "config": {"workload": name, "M": M, "K": K, "N": N, "format": fmt, "hadamard": had},
+        "cpu_baseline": {"value": tflops, "unit": "TFLOP/s", "cores": cores, "kind": "port",
+                         "sample": f"full workload M={M} per step (act-quant + dequant + fp32 matmul)"},
+        "e2e": {"value": tflops, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c1", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    cfg = CONFIGS[args.config]
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, cfg, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2509_23202_b200 as P
+    from paper_2509_23202_b200.quantize import act_quant_into, alloc_result
+    from paper_2509_23202_b200.sharded import gather_columns
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    name, M, K, N, fmt, had = cfg
+    spec = P.FormatSpec.mxfp4() if fmt == "mxfp4" else P.FormatSpec.nvfp4()
+    tr = P.TransformSpec.hadamard(had)
+    g = torch.Generator(device=dev)
+    g.manual_seed(1234)
+    x = torch.randn((M, K), generator=g, device=dev, dtype=torch.float32).bfloat16()
+    g.manual_seed(4321)
+    w_dense = (torch.randn((N, K), generator=g, device=dev, dtype=torch.float32) / K ** 0.5).bfloat16()
+    w_full = P.quantize_weight(w_dense, spec, tr)            # GPU RTN == reference quantize_rtn(W, ..., H)
+    w = w_full.shard(rank, world) if world > 1 else w_full
+    a = alloc_result(M, K, w.fmt, had, dev)
+    y = torch.empty((M, w.N), dtype=torch.bfloat16, device=dev)
+    flush = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    launches_per_step = (1 if fmt == "mxfp4" else 3) + 1   # K1 (+NVFP4 memset + max pass) + K2
+
+    def step():
+        act_quant_into(x, w.fmt, had, a.codes, a.sf, a.tensor_scale_dev, a.scratch)
+        P.gemm(a, w, y)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    # ---------------- device-timed hot path (per-step events, L2 flushed in between)
+    for _ in range(args.warmup):
+        flush.zero_()
+        step()
+    sampler = ClockSampler(torch.cuda.current_device()).start()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    barrier()
+    for i in range(args.steps):
+        flush.zero_()
+        ev[i][0].record(stream)
+        act_quant_into(x, w.fmt, had, a.codes, a.sf, a.tensor_scale_dev, a.scratch)
+        ev[i][1].record(stream)
+        P.gemm(a, w, y)
+        if world > 1:
+            gather_columns(y, None)  # time-to-gathered-output includes the NCCL all-gather
+        ev[i][2].record(stream)
+    barrier()
+    clocks = sampler.stop()
+    t_k1 = [ev[i][0].elapsed_time(ev[i][1]) * 1e-3 for i in range(args.steps)]
+    t_k2 = [ev[i][1].elapsed_time(ev[i][2]) * 1e-3 for i in range(args.steps)]
+    t_step = sum(t_k1) / args.steps + sum(t_k2) / args.steps
+    if world > 1:
+        tt = torch.tensor([t_step], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_step = float(tt.item())
+    flops = 2.0 * M * N * K  # whole job (all ranks together compute the full N)
+    value = flops / t_step / 1e12
+    k1_mean, k2_mean = sum(t_k1) / len(t_k1), sum(t_k2) / len(t_k2)
+
+    # ---------------- cuBLAS bf16 of the same layer (primary comparator)
+    wb = w_dense if world == 1 else w_dense[rank * w.N:(rank + 1) * w.N]
+    yb = torch.empty((M, wb.shape[0]), dtype=torch.bfloat16, device=dev)
+    for _ in range(args.warmup):
+        torch.matmul(x, wb.t(), out=yb)
+    tb = []
+    nb = min(args.steps, 50)
+    for _ in range(nb):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        torch.matmul(x, wb.t(), out=yb)
+        e1.record(stream)
+        tb.append((e0, e1))
+    torch.cuda.synchronize(dev)
+    t_bf16 = sum(e0.elapsed_time(e1) for e0, e1 in tb) / nb * 1e-3
+
+    # ---------------- end to end through the public API, host buffers
+    e2e = None
+    if not args.no_e2e:
+        xh = x.cpu().pin_memory()
+        yh = torch.empty((M, N), dtype=torch.bfloat16).pin_memory()
+        xd = torch.empty_like(x)
+        ne = min(args.steps, 20)
+
+        def e2e_step():
+            xd.copy_(xh, non_blocking=True)
+            if world > 1:
+                yy = P.quantized_linear_sharded(xd, w)
+            else:
+                yy = P.quantized_linear(xd, w)
+            yh.copy_(yy, non_blocking=True)
+
+        for _ in range(3):
+            e2e_step()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(ne):
+            e2e_step()
+        e1.record(stream)
+        barrier()
+        t_e2e = e0.elapsed_time(e1) * 1e-3 / ne
+        if world > 1:
+            tt = torch.tensor([t_e2e], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t_e2e = float(tt.item())
+        e2e = {"value": flops / t_e2e / 1e12, "unit": "TFLOP/s", "ms_per_step": t_e2e * 1e3,
+               "h2d_bytes_per_step": xh.numel() * xh.element_size(),
+               "d2h_bytes_per_step": yh.numel() * yh.element_size()}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    hbm, bf16_burst, bf16_sust, peak_src = peaks()
+    G = 32 if fmt == "mxfp4" else 16
+    k1_bytes = M * K * (2 + 0.5 + 1.0 / G) + (4 if fmt == "nvfp4" else 0)
+    k2_flops = 2.0 * M * w.N * K
+    fp4_peak = 4.0 * bf16_burst
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get(f"{args.config}:k2")
+        except Exception:
+            traffic = None
+
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        Ms = 256  # bounded sample: 256 of the M tokens, same K/N/format
+        import numpy as np
+        X, Wdeq = cpu_inputs(Ms, K, N, fmt, had)
+        cores = len(os.sched_getaffinity(0))
+        cpu_linear_step(X, Wdeq, fmt, had, cores)
+        reps, t0 = 0, time.perf_counter()
+        while reps < 3 or time.perf_counter() - t0 < 5.0:
+            cpu_linear_step(X, Wdeq, fmt, had, cores)
+            reps += 1
+        tc = (time.perf_counter() - t0) / reps
+        cpu = {"value": 2.0 * Ms * N * K / tc / 1e12, "unit": "TFLOP/s", "cores": cores, "kind": "port",
+               "sample": f"M={Ms} of {M} tokens, act-quant + dequant + fp32 matmul, {reps} reps"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "fp4-e2m1 (fp32 accum)",
+        "data": "synthetic: bf16 N(0,1) activations, N(0,1/K) random-init weights (GPU RTN)",
+        "config": {"workload": name, "M": M, "K": K, "N": N, "format": fmt, "hadamard": had,
+                   "parallelism": f"N-shard x{world}" if world > 1 else "single", "l2": "flushed (256 MiB memset) between steps"},
+        "k1_us": k1_mean * 1e6, "k2_us": k2_mean * 1e6,
+        "rotquant_gbs": k1_bytes / k1_mean / 1e9,
+        "bf16_cublas_us": t_bf16 * 1e6, "bf16_cublas_tflops": 2.0 * M * wb.shape[0] * K / t_bf16 / 1e12,
+        "speedup_vs_cublas_bf16": t_bf16 / (k1_mean + k2_mean),
+        "roofline": {"bound": "tensor", "kernel": "k_gemm_fp4 (K2)", "achieved": k2_flops / k2_mean / 1e12,
+                     "peak": fp4_peak, "unit": "TFLOP/s", "frac": k2_flops / k2_mean / 1e12 / fp4_peak,
+                     "peak_note": f"4x {peak_src} bf16 burst {bf16_burst} TF/s (PAPER.md:566 'out of 4x')",
+                     "traffic": traffic},
+        "roofline_k1": {"bound": "hbm", "kernel": "k_act_quant (K1)", "achieved": k1_bytes / k1_mean / 1e9,
+                        "peak": hbm, "unit": "GB/s", "frac": k1_bytes / k1_mean / 1e9 / hbm},
+        "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+        "gpu_launches": launches_per_step * args.steps,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

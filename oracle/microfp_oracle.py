@@ -57,6 +57,8 @@ __all__ = [
     "sf_swizzled_size",
     "mfpq_bytes",
     "bf16_round",
+    "quantize_rtn_parallel",
+    "dequantize_f32",
 ]
 
 MXFP4 = "mxfp4"
@@ -323,3 +325,69 @@ def bf16_round(x) -> np.ndarray:
     u = f.view(np.uint32).astype(np.uint64)
     u = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16) << 16
     return u.astype(np.uint32).view(np.float32).reshape(f.shape)
+
+
+# --- multi-threaded variant used for the CPU baseline (same results, no metrics) ---
+
+def quantize_rtn_parallel(X, fmt: str, hadamard: int | None = None, workers: int | None = None,
+                          rows_per_chunk: int = 64) -> OracleQuant:
+    """``quantize_rtn`` split over row chunks on a thread pool (numpy releases the GIL).
+
+    Identical codes / scales / tensor scale to :func:`quantize_rtn`; the NVFP4
+    whole-tensor max (quantizers.py:198-200) is a reduction over the chunk maxima.
+    Metrics are not computed (mse_rel = mse_top_rel = nan).
+    """
+    import concurrent.futures as cf
+    import os
+
+    G = _format_params(fmt)
+    X = np.asarray(X)
+    rows, cols = X.shape
+    if cols % G or (hadamard and cols % hadamard):
+        raise OracleDataError("columns not divisible by group size / transform block")
+    workers = workers or os.cpu_count() or 1
+    bounds = [(r, min(r + rows_per_chunk, rows)) for r in range(0, rows, rows_per_chunk)]
+    ecodes = np.empty((rows, cols), np.uint8)
+    scodes = np.empty((rows, cols // G), np.uint8)
+    amax = np.empty((rows, cols // G))
+
+    def phase1(b):
+        Xc = np.asarray(X[b[0]:b[1]], dtype=np.float64)
+        if not np.isfinite(Xc).all():
+            raise OracleDataError("non-finite element")
+        Y = rotate_blockwise(Xc, hadamard)
+        amax[b[0]:b[1]] = np.abs(Y.reshape(len(Y), -1, G)).max(axis=2)
+        return Y
+
+    with cf.ThreadPoolExecutor(workers) as ex:
+        Ys = list(ex.map(phase1, bounds))
+        if fmt == NVFP4:
+            top = float(amax.max()) / 6.0
+            s_glob = float(np.float32(top / E4M3_MAX)) if top > 0 else 1.0
+            ts = s_glob
+        else:
+            s_glob, ts = 1.0, FOUR_THIRDS_F32
+
+        def phase2(i):
+            r0, r1 = bounds[i]
+            am = amax[r0:r1]
+            raw = np.where(am == 0.0, 1.0, am / 6.0)
+            if fmt == NVFP4:
+                sc = e4m3_encode(raw / s_glob)
+                dec = E4M3_LEVELS[sc.astype(np.intp)]
+            else:
+                sc = e8m0_encode(raw)
+                dec = np.ldexp(1.0, sc.astype(np.int64) - 127)
+            eff = ts * dec
+            with np.errstate(divide="ignore", invalid="ignore"):
+                u = Ys[i].reshape(r1 - r0, -1, G) / eff[..., None]
+            ecodes[r0:r1] = fp4_codes(u).reshape(r1 - r0, cols)
+            scodes[r0:r1] = sc
+
+        list(ex.map(phase2, range(len(bounds))))
+    return OracleQuant(fmt, rows, cols, G, hadamard or None, ecodes, scodes, ts, float("nan"), float("nan"))
+
+
+def dequantize_f32(q: OracleQuant) -> np.ndarray:
+    """dequantize(q).astype(float32) (formats.py:441 in float64, then cast)."""
+    return dequantize(q).astype(np.float32)
