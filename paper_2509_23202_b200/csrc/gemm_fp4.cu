@@ -68,7 +68,41 @@ struct GemmArgs {
   int64_t sf_col_blocks;  // ceil(K / VEC / 4)
   int64_t b_row_blocks;   // ceil(N / 128)
   int num_m_blk, num_n_blk, num_kb;
+  int debug;  // perf experiments: 1 = no operand loads, 2 = no MMAs (0 in production)
 };
+
+
+// 32 consecutive accumulator columns of one output row -> global (bf16 or f32).
+template <int OUT>
+__device__ __forceinline__ void store_row32(const GemmArgs& g, int64_t row, int64_t col, const uint32_t (&r)[32],
+                                            float alpha) {
+  if constexpr (OUT == MRFP4_DT_BF16) {
+    __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(g.d) + row * g.ldd + col;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (col + 8 * j < g.N) {
+        uint32_t w[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(r[8 * j + 2 * t]) * alpha,
+                                                   __uint_as_float(r[8 * j + 2 * t + 1]) * alpha);
+          w[t] = *reinterpret_cast<uint32_t*>(&h);
+        }
+        *reinterpret_cast<uint4*>(dst + 8 * j) = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+    }
+  } else {
+    float* dst = static_cast<float*>(g.d) + row * g.ldd + col;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (col + 4 * j < g.N) {
+        *reinterpret_cast<float4*>(dst + 4 * j) =
+            make_float4(__uint_as_float(r[4 * j]) * alpha, __uint_as_float(r[4 * j + 1]) * alpha,
+                        __uint_as_float(r[4 * j + 2]) * alpha, __uint_as_float(r[4 * j + 3]) * alpha);
+      }
+    }
+  }
+}
 
 template <int VEC, int BN, int OUT>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -116,6 +150,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int j = 0; j < C::kNB; ++j) nbv += ((int64_t)n_blk * C::kNB + j < g.b_row_blocks);
           const uint32_t bytes = C::kABytes + C::kBBytes + (uint32_t)atoms * 512u * (1u + nbv);
+          if (g.debug == 1 || g.debug == 3 || g.debug == 4) {
+            sm100::mbar_arrive(&full[stage]);
+            if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+            continue;
+          }
           sm100::mbar_arrive_expect_tx(&full[stage], bytes);
           sm100::tma_load_2d(smem + C::kOffA + stage * C::kABytes, &tmA, &full[stage], kb * BK_BYTES, m_blk * BM);
           sm100::tma_load_2d(smem + C::kOffB + stage * C::kBBytes, &tmB, &full[stage], kb * BK_BYTES, n_blk * BN);
@@ -159,7 +198,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t a_s = sm100::smem_u32(smem + C::kOffA + stage * C::kABytes);
           const uint32_t b_s = sm100::smem_u32(smem + C::kOffB + stage * C::kBBytes);
           const int nk = (int)imin64(BK / UMMA_K, (g.K - (int64_t)kb * BK) / UMMA_K);
-          for (int k = 0; k < nk; ++k) {
+          for (int k = 0; k < ((g.debug == 2 || g.debug == 4) ? 0 : nk); ++k) {
             const int atom = VEC == 16 ? k : (k >> 1);
             const uint32_t sfid = VEC == 16 ? 0u : (uint32_t)(k & 1) * 2u;
             const uint64_t adesc = sm100::smem_desc(a_s + k * (UMMA_K / 2), 16, 1024, 2);
@@ -186,39 +225,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       sm100::tc_fence_after();
       const int64_t row = (int64_t)m_blk * BM + q * 32 + lane;
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
+      for (int c = 0; c < (g.debug >= 3 ? 0 : BN); c += 32) {
         uint32_t r[32];
         sm100::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + c, r);
         sm100::tmem_ld_wait();
         const int64_t col = (int64_t)n_blk * BN + c;
-        if (row < g.M) {
-          if constexpr (OUT == MRFP4_DT_BF16) {
-            __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(g.d) + row * g.ldd + col;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              if (col + 8 * j < g.N) {
-                uint32_t w[4];
-#pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                  __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(r[8 * j + 2 * t]) * alpha,
-                                                           __uint_as_float(r[8 * j + 2 * t + 1]) * alpha);
-                  w[t] = *reinterpret_cast<uint32_t*>(&h);
-                }
-                *reinterpret_cast<uint4*>(dst + 8 * j) = make_uint4(w[0], w[1], w[2], w[3]);
-              }
-            }
-          } else {
-            float* dst = static_cast<float*>(g.d) + row * g.ldd + col;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              if (col + 4 * j < g.N) {
-                *reinterpret_cast<float4*>(dst + 4 * j) =
-                    make_float4(__uint_as_float(r[4 * j]) * alpha, __uint_as_float(r[4 * j + 1]) * alpha,
-                                __uint_as_float(r[4 * j + 2]) * alpha, __uint_as_float(r[4 * j + 3]) * alpha);
-              }
-            }
-          }
-        }
+        if (row < g.M) store_row32<OUT>(g, row, col, r, alpha);
       }
       sm100::tc_fence_before();
       __syncwarp();
@@ -230,6 +242,178 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) {
     sm100::tc_fence_after();
     sm100::tmem_dealloc(tmem_base, C::kTmemCols);
+  }
+}
+
+
+// ---------------------------------------------------------------------------
+// 2-CTA (cta_group::2) variant: a CTA pair computes a 256 x 256 tile.  Each CTA
+// TMA-loads its own 128 rows of A and 128 rows of B (the pair's MMA reads B from
+// both SMEMs), its SFA and the full 256-row SFB; completion bytes of both CTAs
+// land on the leader's mbarrier.  The leader's single thread issues
+// tcgen05.cp/.mma with cta_group::2 and commits (multicast) to both CTAs' empty /
+// tmem-full barriers.  Halves the L2->SMEM bytes per MMA of the 1-CTA kernel.
+// ---------------------------------------------------------------------------
+template <int VEC>
+struct Cfg2 {
+  static constexpr int kAtomsPerKb = BK / VEC / 4;
+  static constexpr int kStages = VEC == 16 ? 5 : 6;
+  static constexpr int kABytes = 128 * BK_BYTES;
+  static constexpr int kBBytes = 128 * BK_BYTES;
+  static constexpr int kSfaBytes = kAtomsPerKb * 512;
+  static constexpr int kSfbBytes = 2 * kAtomsPerKb * 512;
+  static constexpr int kStageBytes = kABytes + kBBytes + kSfaBytes + kSfbBytes;
+  static constexpr int kSfaCols = kAtomsPerKb * 4;
+  static constexpr int kSfbCols = 2 * kAtomsPerKb * 4;
+  static constexpr int kSfSlots = 2;
+  static constexpr int kAccCols = 256;
+  static constexpr int kTmemCols = 512;
+  static_assert(kAccCols + kSfSlots * (kSfaCols + kSfbCols) <= kTmemCols, "TMEM budget");
+  static constexpr int kOffA = 0;
+  static constexpr int kOffB = kOffA + kStages * kABytes;
+  static constexpr int kOffSfa = kOffB + kStages * kBBytes;
+  static constexpr int kOffSfb = kOffSfa + kStages * kSfaBytes;
+  static constexpr int kOffBar = kOffSfb + kStages * kSfbBytes;
+  static constexpr int kSmem = kOffBar + 256 + 1024;
+};
+
+template <int VEC, int OUT>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    k_gemm_fp4_2sm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ CUtensorMap tmSFA, const __grid_constant__ CUtensorMap tmSFB, GemmArgs g) {
+  using C = Cfg2<VEC>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
+  uint64_t* empty = full + C::kStages;
+  uint64_t* tfull = empty + C::kStages;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 1);
+
+  const uint32_t rank = sm100::cluster_ctarank();
+  const bool leader = rank == 0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    sm100::tma_prefetch_desc(&tmA);
+    sm100::tma_prefetch_desc(&tmB);
+    sm100::tma_prefetch_desc(&tmSFA);
+    sm100::tma_prefetch_desc(&tmSFB);
+    for (int s = 0; s < C::kStages; ++s) {
+      sm100::mbar_init(&full[s], 1);
+      sm100::mbar_init(&empty[s], 1);
+    }
+    sm100::mbar_init(tfull, 1);
+    sm100::mbar_init(tempty, 8);  // 4 epilogue warps x 2 CTAs
+    sm100::fence_mbar_init();
+  }
+  if (warp == 1) sm100::tmem_alloc_2sm(tmem_holder, C::kTmemCols);
+  sm100::tc_fence_before();
+  __syncwarp();
+  sm100::cluster_sync();
+  sm100::tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  const int num_tiles = g.num_m_blk * g.num_n_blk;  // 256 x 256 tiles
+  const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------------------------------------------- producer (both CTAs)
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = cluster; tile < num_tiles; tile += nclusters) {
+        const int m_blk = tile % g.num_m_blk, n_blk = tile / g.num_m_blk;
+        for (int kb = 0; kb < g.num_kb; ++kb) {
+          sm100::mbar_wait(&empty[stage], phase ^ 1);
+          if (leader) sm100::mbar_arrive_expect_tx(&full[stage], 2u * C::kStageBytes);
+          const uint32_t lb = sm100::leader_bar(&full[stage]);
+          sm100::tma_load_2d_2sm(smem + C::kOffA + stage * C::kABytes, &tmA, lb, kb * BK_BYTES,
+                                 m_blk * 256 + (int)rank * 128);
+          sm100::tma_load_2d_2sm(smem + C::kOffB + stage * C::kBBytes, &tmB, lb, kb * BK_BYTES,
+                                 n_blk * 256 + (int)rank * 128);
+          sm100::tma_load_2d_2sm(smem + C::kOffSfa + stage * C::kSfaBytes, &tmSFA, lb, kb * C::kAtomsPerKb * 64,
+                                 m_blk * 2 + (int)rank);
+          sm100::tma_load_2d_2sm(smem + C::kOffSfb + stage * C::kSfbBytes, &tmSFB, lb, kb * C::kAtomsPerKb * 64,
+                                 n_blk * 2);
+          if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      // ------------------------------------------------ MMA issuer (leader only)
+      int stage = 0;
+      uint32_t phase = 0, acc_phase = 0, kbg = 0;
+      for (int tile = cluster; tile < num_tiles; tile += nclusters) {
+        sm100::mbar_wait(tempty, acc_phase ^ 1);
+        sm100::tc_fence_after();
+        for (int kb = 0; kb < g.num_kb; ++kb, ++kbg) {
+          sm100::mbar_wait(&full[stage], phase);
+          sm100::tc_fence_after();
+          const uint32_t sfa_t = tmem_base + C::kAccCols + (kbg & 1) * (C::kSfaCols + C::kSfbCols);
+          const uint32_t sfb_t = sfa_t + C::kSfaCols;
+          const uint32_t sfa_s = sm100::smem_u32(smem + C::kOffSfa + stage * C::kSfaBytes);
+          const uint32_t sfb_s = sm100::smem_u32(smem + C::kOffSfb + stage * C::kSfbBytes);
+#pragma unroll
+          for (int a = 0; a < C::kAtomsPerKb; ++a) {
+            sm100::tc_cp_32x128b_warpx4_2sm(sfa_t + a * 4, sm100::smem_desc(sfa_s + a * 512, 0, 128, 0));
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+              sm100::tc_cp_32x128b_warpx4_2sm(sfb_t + a * 8 + j * 4,
+                                              sm100::smem_desc(sfb_s + (j * C::kAtomsPerKb + a) * 512, 0, 128, 0));
+          }
+          const uint32_t a_s = sm100::smem_u32(smem + C::kOffA + stage * C::kABytes);
+          const uint32_t b_s = sm100::smem_u32(smem + C::kOffB + stage * C::kBBytes);
+          const int nk = (int)imin64(BK / UMMA_K, (g.K - (int64_t)kb * BK) / UMMA_K);
+          for (int k = 0; k < nk; ++k) {
+            const int atom = VEC == 16 ? k : (k >> 1);
+            const uint32_t sfid = VEC == 16 ? 0u : (uint32_t)(k & 1) * 2u;
+            const uint64_t adesc = sm100::smem_desc(a_s + k * (UMMA_K / 2), 16, 1024, 2);
+            const uint64_t bdesc = sm100::smem_desc(b_s + k * (UMMA_K / 2), 16, 1024, 2);
+            const uint32_t idesc = sm100::idesc_fp4(256, 256, VEC == 32, sfid, sfid);
+            sm100::tc_mma_fp4_2sm<VEC>(tmem_base, adesc, bdesc, idesc, (sfa_t + atom * 4) | (sfid << 30),
+                                       (sfb_t + atom * 8) | (sfid << 30), (kb | k) != 0);
+          }
+          sm100::tc_commit_2sm_mc(&empty[stage], 0x3);
+          if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+        }
+        sm100::tc_commit_2sm_mc(tfull, 0x3);
+        acc_phase ^= 1;
+      }
+    }
+  } else {
+    // ------------------------------------------------------ epilogue (both CTAs)
+    const int q = warp & 3;
+    const float alpha = __ldg(g.a_ts) * __ldg(g.b_ts);
+    uint32_t acc_phase = 0;
+    for (int tile = cluster; tile < num_tiles; tile += nclusters) {
+      const int m_blk = tile % g.num_m_blk, n_blk = tile / g.num_m_blk;
+      sm100::mbar_wait(tfull, acc_phase);
+      sm100::tc_fence_after();
+      const int64_t row = (int64_t)m_blk * 256 + rank * 128 + q * 32 + lane;
+#pragma unroll 1
+      for (int c = 0; c < 256; c += 32) {
+        uint32_t r[32];
+        sm100::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + c, r);
+        sm100::tmem_ld_wait();
+        const int64_t col = (int64_t)n_blk * 256 + c;
+        if (row < g.M) store_row32<OUT>(g, row, col, r, alpha);
+      }
+      sm100::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (leader) sm100::mbar_arrive(tempty);
+        else sm100::mbar_arrive_remote(tempty, 0);
+      }
+      acc_phase ^= 1;
+    }
+  }
+  sm100::tc_fence_before();
+  __syncwarp();
+  sm100::cluster_sync();
+  if (warp == 1) {
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc_2sm(tmem_base, C::kTmemCols);
   }
 }
 
@@ -256,6 +440,21 @@ bool make_code_map(CUtensorMap* tm, const uint8_t* ptr, int64_t rows, int64_t K,
   cuuint32_t estr[2] = {1, 1};
   CUresult r = encode(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(ptr), dims, strides, box, estr,
                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// Swizzled scale factors viewed as [128-row blocks][col_blocks * 64] uint64 (one 512-B atom = 64 x u64).
+bool make_sf_map(CUtensorMap* tm, const uint8_t* sf, int64_t rows, int64_t sf_cols, int atoms, int box_rows) {
+  auto encode = get_encode_fn();
+  if (!encode) return false;
+  const int64_t rb = ceil_div(rows, 128), cb = ceil_div(sf_cols, 4);
+  cuuint64_t dims[2] = {(cuuint64_t)(cb * 64), (cuuint64_t)rb};
+  cuuint64_t strides[1] = {(cuuint64_t)(cb * 512)};
+  cuuint32_t box[2] = {(cuuint32_t)(atoms * 64), (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode(tm, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<uint8_t*>(sf), dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -295,12 +494,44 @@ int launch(const uint8_t* a, const uint8_t* b, const GemmArgs& args0, cudaStream
   return cudaPeekAtLastError() == cudaSuccess ? MRFP4_OK : MRFP4_ECUDA;
 }
 
+template <int VEC, int OUT>
+int launch2(const uint8_t* a, const uint8_t* b, const GemmArgs& args0, cudaStream_t s) {
+  using C = Cfg2<VEC>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(k_gemm_fp4_2sm<VEC, OUT>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem) !=
+        cudaSuccess)
+      return MRFP4_ECUDA;
+    attr_set = true;
+  }
+  GemmArgs g = args0;
+  CUtensorMap tmA, tmB, tmSFA, tmSFB;
+  const int64_t sfc = g.K / VEC;
+  if (!make_code_map(&tmA, a, g.M, g.K, 128) || !make_code_map(&tmB, b, g.N, g.K, 128) ||
+      !make_sf_map(&tmSFA, g.a_sf, g.M, sfc, C::kAtomsPerKb, 1) ||
+      !make_sf_map(&tmSFB, g.b_sf, g.N, sfc, C::kAtomsPerKb, 2))
+    return MRFP4_ECUDA;
+  g.num_m_blk = (int)ceil_div(g.M, 256);
+  g.num_n_blk = (int)ceil_div(g.N, 256);
+  g.num_kb = (int)ceil_div(g.K, BK);
+  g.sf_col_blocks = ceil_div(sfc, 4);
+  g.b_row_blocks = ceil_div(g.N, 128);
+  const int tiles = g.num_m_blk * g.num_n_blk;
+  const int clusters = std::min(tiles, num_sms() / 2);
+  k_gemm_fp4_2sm<VEC, OUT><<<2 * clusters, kThreads, C::kSmem, s>>>(tmA, tmB, tmSFA, tmSFB, g);
+  return cudaPeekAtLastError() == cudaSuccess ? MRFP4_OK : MRFP4_ECUDA;
+}
+
 }  // namespace
+
+int g_debug_mode = 0;
+int g_force_kernel = 0;  // 0 auto, 1 = 1-CTA kernel, 2 = 2-CTA kernel
 
 int launch_gemm_fp4(const uint8_t* a, const uint8_t* a_sf, const float* a_ts, const uint8_t* b, const uint8_t* b_sf,
                     const float* b_ts, void* d, int d_dtype, int64_t M, int64_t N, int64_t K, int64_t ldd, int fmt,
                     cudaStream_t s) {
   GemmArgs g{};
+  g.debug = g_debug_mode;
   g.a_sf = a_sf;
   g.b_sf = b_sf;
   g.a_ts = a_ts;
@@ -310,6 +541,12 @@ int launch_gemm_fp4(const uint8_t* a, const uint8_t* a_sf, const float* a_ts, co
   g.N = N;
   g.K = K;
   g.ldd = ldd;
+  const bool pair = g_force_kernel ? g_force_kernel == 2 : M > 128;
+  if (pair) {
+    if (fmt == MRFP4_FMT_NVFP4)
+      return d_dtype == MRFP4_DT_BF16 ? launch2<16, MRFP4_DT_BF16>(a, b, g, s) : launch2<16, MRFP4_DT_F32>(a, b, g, s);
+    return d_dtype == MRFP4_DT_BF16 ? launch2<32, MRFP4_DT_BF16>(a, b, g, s) : launch2<32, MRFP4_DT_F32>(a, b, g, s);
+  }
   if (fmt == MRFP4_FMT_NVFP4) {
     return d_dtype == MRFP4_DT_BF16 ? launch<16, 256, MRFP4_DT_BF16>(a, b, g, s)
                                     : launch<16, 256, MRFP4_DT_F32>(a, b, g, s);
@@ -319,3 +556,16 @@ int launch_gemm_fp4(const uint8_t* a, const uint8_t* a_sf, const float* a_ts, co
 }
 
 }  // namespace mrfp4
+
+// Perf experiments only (deliberately not in include/mrfp4.h): 1 = skip operand loads, 2 = skip MMAs.
+extern "C" int mrfp4_debug_gemm_kernel(int which) {
+  const int old = mrfp4::g_force_kernel;
+  mrfp4::g_force_kernel = which;
+  return old;
+}
+
+extern "C" int mrfp4_debug_gemm_mode(int mode) {
+  const int old = mrfp4::g_debug_mode;
+  mrfp4::g_debug_mode = mode;
+  return old;
+}

@@ -56,10 +56,23 @@ def rel_fro(y, ref):
     return float(np.linalg.norm(y - ref) / max(np.linalg.norm(ref), 1e-300))
 
 
+@pytest.fixture(params=[1, 2], ids=["cta1", "cta2"])
+def kernel(request):
+    """Force the 1-CTA or the 2-CTA (cta_group::2) GEMM kernel for this test."""
+    import ctypes
+    from paper_2509_23202_b200 import _lib
+    fn = _lib.lib().mrfp4_debug_gemm_kernel
+    fn.argtypes = [ctypes.c_int]
+    old = fn(request.param)
+    yield request.param
+    fn(old)
+
+
 @pytest.mark.parametrize("fmt", ["mxfp4", "nvfp4"])
 @pytest.mark.parametrize("M,N,K", [
-    (128, 256, 256), (1, 256, 64), (16, 512, 4096), (200, 384, 1024), (300, 264, 192), (512, 1024, 2048)])
-def test_gemm_random_codes_fp32(fmt, M, N, K):
+    (128, 256, 256), (1, 256, 64), (16, 512, 4096), (200, 384, 1024), (300, 264, 192), (512, 1024, 2048),
+    (640, 768, 1280)])
+def test_gemm_random_codes_fp32(fmt, M, N, K, kernel):
     rng = np.random.default_rng(M * 131 + N * 7 + K)
     A, W = random_container(rng, M, K, fmt), random_container(rng, N, K, fmt)
     y = run_gemm(A, W).cpu().numpy()
