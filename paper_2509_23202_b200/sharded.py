@@ -31,9 +31,9 @@ def gather_columns(y_shard: torch.Tensor, group=None) -> torch.Tensor:
     if world == 1:
         return y_shard
     M, n = y_shard.shape
-    buf = torch.empty((world, M, n), dtype=y_shard.dtype, device=y_shard.device)
+    buf = torch.empty((world * M, n), dtype=y_shard.dtype, device=y_shard.device)  # rank-major [P*M, N/P]
     dist.all_gather_into_tensor(buf, y_shard.contiguous(), group=group)
-    return buf.permute(1, 0, 2).reshape(M, world * n)
+    return buf.view(world, M, n).permute(1, 0, 2).reshape(M, world * n)
 
 
 def quantized_linear_sharded(x: torch.Tensor, w_shard: PackedWeight, group=None, *,
