@@ -7,8 +7,11 @@ against RTN weights prepared once).  Default workload = BASELINE.json configs[1]
 Llama-3-8B MLP down_proj, K=14336 -> N=4096, 2048 tokens, MXFP4 + Hadamard-32.
 
 Reported (one JSON line from rank 0):
-  value / ms_per_step   FP4-linear TFLOP/s = 2*M*N*K / (t_K1 + t_K2), device time,
-                        inputs resident in HBM, L2 flushed (256 MiB memset) between steps
+  value / ms_per_step   FP4-linear TFLOP/s = 2*M*N*K / t_step, t_step = CUDA events around K1+K2
+                        (back to back, PDL overlaps K2's prologue with K1's tail), inputs resident
+                        in HBM, L2 flushed between steps: a 256 MiB memset, then a 256 MiB read
+                        sweep of a second buffer so the flush's dirty lines are written back
+                        outside the timed region
   e2e                   same metric through the public API (quantized_linear) with the
                         activations copied from pinned host memory and Y read back per step
   roofline              dominant kernel (K2) vs 4x the measured bf16 peak; K1 vs measured HBM
@@ -70,7 +73,7 @@ class ClockSampler:
         try:
             self.fh = open(self.path, "w")
             self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "50",
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "20",
                  "-i", str(self.dev)], stdout=self.fh, stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
@@ -145,8 +148,8 @@ def run_reference(args, cfg, rank):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c1", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -187,48 +190,61 @@ def main():
     w = w_full.shard(rank, world) if world > 1 else w_full
     a = alloc_result(M, K, w.fmt, had, dev)
     y = torch.empty((M, w.N), dtype=torch.bfloat16, device=dev)
-    flush = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device=dev)
+    flush_w = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device=dev)
+    flush_r = torch.ones(64 * 2 ** 20, dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream(dev)
 
-    launches_per_step = (1 if fmt == "mxfp4" else 3) + 1   # K1 (+NVFP4 memset + max pass) + K2
+    def flush_l2():
+        flush_w.zero_()                    # write a buffer larger than L2 (126 MB) ...
+        flush_r.sum(dtype=torch.int32)     # ... then read another: L2 left clean, none of our data
+
+    launches_per_step = (1 if fmt == "mxfp4" else 2) + 1   # K1 (NVFP4: tensor-max pass + encode pass) + K2
 
     def step():
         act_quant_into(x, w.fmt, had, a.codes, a.sf, a.tensor_scale_dev, a.scratch)
         P.gemm(a, w, y)
+        if world > 1:
+            gather_columns(y, None)  # time-to-gathered-output includes the NCCL all-gather
 
     def barrier():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize(dev)
 
-    # ---------------- device-timed hot path (per-step events, L2 flushed in between)
+    # ---------------- device-timed hot path (L2 flushed before every step)
+    def timed(fn, n):
+        """Per-iteration device times (s) of fn, CUDA events on the launching stream."""
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
+        for e0, e1 in ev:
+            flush_l2()
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+        return ev
+
     for _ in range(args.warmup):
-        flush.zero_()
+        flush_l2()
         step()
     sampler = ClockSampler(torch.cuda.current_device()).start()
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
     barrier()
-    for i in range(args.steps):
-        flush.zero_()
-        ev[i][0].record(stream)
-        act_quant_into(x, w.fmt, had, a.codes, a.sf, a.tensor_scale_dev, a.scratch)
-        ev[i][1].record(stream)
-        P.gemm(a, w, y)
-        if world > 1:
-            gather_columns(y, None)  # time-to-gathered-output includes the NCCL all-gather
-        ev[i][2].record(stream)
+    ev_step = timed(step, args.steps)              # the timed region: exactly K steps
     barrier()
     clocks = sampler.stop()
-    t_k1 = [ev[i][0].elapsed_time(ev[i][1]) * 1e-3 for i in range(args.steps)]
-    t_k2 = [ev[i][1].elapsed_time(ev[i][2]) * 1e-3 for i in range(args.steps)]
-    t_step = sum(t_k1) / args.steps + sum(t_k2) / args.steps
+    t_steps = [a.elapsed_time(b) * 1e-3 for a, b in ev_step]
+    t_step = sum(t_steps) / args.steps
+    # per-kernel split (same inputs, separate untimed-for-value loops) for the rooflines
+    nk = min(args.steps, 50)
+    ev_k1 = timed(lambda: act_quant_into(x, w.fmt, had, a.codes, a.sf, a.tensor_scale_dev, a.scratch), nk)
+    ev_k2 = timed(lambda: P.gemm(a, w, y), nk)
+    torch.cuda.synchronize(dev)
+    k1_mean = sum(a_.elapsed_time(b_) for a_, b_ in ev_k1) / nk * 1e-3
+    k2_mean = sum(a_.elapsed_time(b_) for a_, b_ in ev_k2) / nk * 1e-3
     if world > 1:
         tt = torch.tensor([t_step], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_step = float(tt.item())
     flops = 2.0 * M * N * K  # whole job (all ranks together compute the full N)
     value = flops / t_step / 1e12
-    k1_mean, k2_mean = sum(t_k1) / len(t_k1), sum(t_k2) / len(t_k2)
 
     # ---------------- cuBLAS bf16 of the same layer (primary comparator, BASELINE.md section 4)
     wb = w_dense if world == 1 else w_dense[rank * w.N:(rank + 1) * w.N]
@@ -238,7 +254,7 @@ def main():
     tb = []
     nb = min(args.steps, 50)
     for _ in range(nb):
-        flush.zero_()
+        flush_l2()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         torch.matmul(x, wb.t(), out=yb)
@@ -320,11 +336,11 @@ def main():
         "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "fp4-e2m1 (fp32 accum)",
         "data": "synthetic: bf16 N(0,1) activations, N(0,1/K) random-init weights (GPU RTN)",
         "config": {"workload": name, "M": M, "K": K, "N": N, "format": fmt, "hadamard": had,
-                   "parallelism": f"N-shard x{world}" if world > 1 else "single", "l2": "flushed (256 MiB memset) between steps"},
+                   "parallelism": f"N-shard x{world}" if world > 1 else "single", "l2": "flushed between steps (256 MiB memset + 256 MiB read sweep)"},
         "k1_us": k1_mean * 1e6, "k2_us": k2_mean * 1e6,
         "rotquant_gbs": k1_bytes / k1_mean / 1e9,
         "bf16_cublas_us": t_bf16 * 1e6, "bf16_cublas_tflops": 2.0 * M * wb.shape[0] * K / t_bf16 / 1e12,
-        "speedup_vs_cublas_bf16": t_bf16 / (k1_mean + k2_mean),
+        "speedup_vs_cublas_bf16": t_bf16 / t_step,
         "roofline": {"bound": "tensor", "kernel": "k_gemm_fp4 (K2)", "achieved": k2_flops / k2_mean / 1e12,
                      "peak": fp4_peak, "unit": "TFLOP/s", "frac": k2_flops / k2_mean / 1e12 / fp4_peak,
                      "peak_note": f"4x {peak_src} bf16 burst {bf16_burst} TF/s (PAPER.md:566 'out of 4x')",

@@ -73,7 +73,9 @@ int mrfp4_group_size(int fmt);
 /* Bytes of a swizzled scale-factor buffer for a [rows, sf_cols] scale matrix. */
 size_t mrfp4_sf_bytes(int64_t rows, int64_t sf_cols);
 
-/* Device workspace needed by mrfp4_act_quant (NVFP4 needs 4 bytes for the tensor max). */
+/* Device workspace needed by mrfp4_act_quant (NVFP4: 8 bytes, the tensor max and an
+ * arrival counter).  It must be zero-filled once before first use; every successful
+ * call leaves it zeroed again, so one workspace serves a stream's calls in order. */
 size_t mrfp4_act_quant_workspace(int64_t M, int64_t K, int fmt);
 
 /*
@@ -83,6 +85,8 @@ size_t mrfp4_act_quant_workspace(int64_t M, int64_t K, int fmt);
  * x: [M, K] with row stride ldx elements (ldx*elt_size % 16 == 0), dtype x_dtype.
  * tensor_scale: device float, receives f32(4/3) (MXFP4) or the NVFP4 global scale.
  * NVFP4 runs two stream-ordered passes (whole-tensor max, then encode).
+ * Kernels are launched with programmatic dependent launch (PDL); set MRFP4_PDL=0 in
+ * the environment to launch them with plain stream ordering.
  */
 int mrfp4_act_quant(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ldx,
                     int fmt, int had_k,

@@ -9,20 +9,33 @@
 //   elements quantizers.py:211-215 + formats.py:94-113  RNE onto E2M1, -0 -> 0
 //   packing  formats.py:377-382    low nibble = even element
 //
-// Work decomposition: one thread owns 32 contiguous elements of one row
-// (4 x 16-byte loads for bf16).  Hadamard blocks of k <= 32 are rotated fully in
-// registers; k = 64 / 128 add one / two butterfly stages across 2 / 4 lanes.
-// A CTA covers 64 rows x 128 columns (4 threads per row).
+// Work decomposition (HBM-bound kernel; 2.5 + 1/G bytes per bf16 element):
+//   * A lane owns one 32-element column segment of one row, held as 16 packed pairs
+//     P[j] = (v[2j], v[2j+1]) -- exactly the (low, high) halves of the j-th bf16x2
+//     input word and the two nibbles of the j-th output byte.  FWHT stage h = 1 is the
+//     in-pair butterfly (one FFMA2 with broadcast operands), stages h = 2..16 and the
+//     cross-lane stages are FADD2 / FFMA2 between pairs, the group scaling is FMUL2.
+//   * A warp item is 32 segments: L = 2^ceil(log2(K/32)) lanes (<= 32) cover a row
+//     chunk, so short rows pack several rows per warp.  Hadamard blocks of k <= 32
+//     rotate in registers; k = 64 / 128 add 1 / 2 shuffle stages across lane bits 0 / 1.
+//   * Persistent grid; each warp walks a contiguous range of items with incremental
+//     (row, segment) cursors, each lane streaming its segments through a private
+//     3-stage cp.async ring in shared memory (16-B chunks XOR-swizzled by lane, so the
+//     16-B shared loads are bank-conflict free) -- no block barriers on the data path.
+//   * Scale codes go straight into the swizzled tensor-core layout, codes out as one
+//     16-B store per segment.
 //
 // Exactness: the rotation is an fp32 FWHT (exact whenever the block sum fits in
-// 24 bits -- always for k in {16, 64} scaling, typically for bf16 inputs).  All
-// downstream decisions reproduce the reference's float64 arithmetic on the
-// rotated value y = S * c:  scale codes are decided from an fp32 estimate and
-// re-decided in float64 whenever the estimate is within 2^-18 of a rounding
-// threshold; element codes are decided twice with u*(1 +- 2^-18) and any element
-// whose two roundings disagree is re-decided from u = RN64(y / eff) exactly as
-// numpy does (quantizers.py:213).
+// 24 bits; validated by the parity tests).  All downstream decisions reproduce the
+// reference's float64 arithmetic on the rotated value y = S * c:  scale codes are
+// decided from an fp32 estimate and re-decided in float64 whenever the estimate is
+// within 2^-17 of a rounding threshold; element codes are rounded twice through the
+// hardware E2M1 conversion, from u * (1 +- 2^-18) (the fp32 u ~ y / eff is within
+// 2^-21 of the exact quotient), and any element whose two roundings disagree is
+// re-decided from u = RN64(y / eff) exactly as numpy does (quantizers.py:213).
 #include <algorithm>
+#include <cstring>
+#include <mutex>
 
 #include "common.cuh"
 
@@ -30,10 +43,19 @@ namespace mrfp4 {
 
 namespace {
 
-constexpr int kSeg = 32;
-constexpr int kSegsPerRow = 4;
-constexpr int kRowsPerCta = 64;
-constexpr int kThreads = kRowsPerCta * kSegsPerRow;  // 256
+constexpr int kSeg = 32;       // elements per lane segment
+constexpr int kPairs = kSeg / 2;
+constexpr int kWarps = 8;      // warps per CTA
+constexpr int kThreads = kWarps * 32;
+constexpr int kStages = 3;     // cp.async ring depth per lane
+
+template <int IN>
+struct InCfg {
+  static constexpr int kEs = IN == MRFP4_DT_F32 ? 4 : 2;
+  static constexpr int kChunks = kSeg * kEs / 16;          // 16-B chunks per segment: 4 or 8
+  static constexpr int kLaneBytes = kSeg * kEs;
+  static constexpr int kSmem = kWarps * kStages * 32 * kLaneBytes;
+};
 
 struct AQParams {
   const void* x;
@@ -46,113 +68,212 @@ struct AQParams {
   int64_t sf_cols;         // K / G
   int64_t sf_col_blocks;   // ceil(sf_cols / 4)
   int64_t rows_pad;        // ceil(M / 128) * 128
+  int64_t items;           // warp items
+  int nchunk;              // column chunks of L segments per row group
+  int seg_span;            // nchunk * L
+  int lane_bits;           // log2(L)
   double c64;              // RN64(1 / RN64(sqrt(k)))  (transforms.py:65: H / np.sqrt(k))
-  float c32;
+  float kraw;              // MXFP4: ~ c / 6
+  float kmx;               // MXFP4: ~ c / f32(4/3)
+  unsigned long long pm;   // f32x2 (1, -1): FWHT h = 1 signs, a uniform-register operand of FFMA2
+  int Mi, Ki;              // M, K as 32-bit (the C-ABI checks they fit)
+  uint32_t half_k;         // K / 2: bytes per code row
+  uint32_t cb;             // sf_col_blocks as 32-bit
 };
 
 // ---------------------------------------------------------------------------
-// loads
+// packed f32x2 helpers (sm_100a FADD2 / FMUL2 / FFMA2)
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void bf16x2_to_f32(uint32_t w, float& lo, float& hi) {
-  lo = __uint_as_float(w << 16);
-  hi = __uint_as_float(w & 0xFFFF0000u);
+typedef unsigned long long u64;
+
+__device__ __forceinline__ u64 pk(float lo, float hi) {
+  u64 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ float lo_of(u64 v) { return __uint_as_float((uint32_t)v); }
+__device__ __forceinline__ float hi_of(u64 v) { return __uint_as_float((uint32_t)(v >> 32)); }
+__device__ __forceinline__ u64 add2(u64 a, u64 b) {
+  u64 r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ u64 sub2(u64 a, u64 b) {
+  u64 r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ u64 mul2(u64 a, u64 b) {
+  u64 r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ u64 fma2(u64 a, u64 b, u64 c) {
+  u64 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+// max(|a|, |b|, |c|), NaN-propagating (a NaN anywhere in a group must reach the status check)
+__device__ __forceinline__ float amax3(float a, float b, float c) {
+  float r;
+  asm("max.NaN.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(fabsf(a)), "f"(fabsf(b)), "f"(fabsf(c)));
+  return r;
+}
+__device__ __forceinline__ float max3n(float a, float b, float c) {
+  float r;
+  asm("max.NaN.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+// cp.async ring
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g, uint32_t bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(saddr), "l"(g), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ uint4 lds128(uint32_t saddr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(saddr));
+  return v;
+}
+
+// Physical 16-B chunk of logical chunk j in a lane's ring slot: XOR-swizzled so the
+// eight lanes of a quarter warp hit eight different 16-B bank groups on a 16-B load.
+template <int IN>
+__device__ __forceinline__ uint32_t swz(int j, int lane) {
+  return InCfg<IN>::kChunks == 8 ? (uint32_t)(j ^ (lane & 7)) : (uint32_t)(j ^ ((lane >> 1) & 3));
+}
+
+// A lane's position: row and 32-element column segment of the current warp item.
+// Items are row-group-major (item = rg * nchunk + cc); a warp walks a contiguous range.
+struct Cursor {
+  int row;
+  int seg;
+};
+
+__device__ __forceinline__ Cursor cursor_at(const AQParams& p, int64_t item, int lane) {
+  const int64_t rg = item / p.nchunk;
+  const int cc = (int)(item - rg * p.nchunk);
+  Cursor c;
+  c.row = (int)(rg * (32 >> p.lane_bits)) + (lane >> p.lane_bits);
+  c.seg = (cc << p.lane_bits) + (lane & ((1 << p.lane_bits) - 1));
+  return c;
+}
+
+template <int DIR>
+__device__ __forceinline__ void cursor_step(const AQParams& p, Cursor& c) {
+  if constexpr (DIR > 0) {
+    c.seg += 1 << p.lane_bits;
+    if (c.seg >= p.seg_span) { c.seg -= p.seg_span; c.row += 32 >> p.lane_bits; }
+  } else {
+    c.seg -= 1 << p.lane_bits;
+    if (c.seg < 0) { c.seg += p.seg_span; c.row -= 32 >> p.lane_bits; }
+  }
 }
 
 template <int IN>
-__device__ __forceinline__ void load_seg(const void* base, int64_t off, int nvalid, float (&v)[kSeg]) {
-  if (nvalid == 0) {
+__device__ __forceinline__ void issue_seg(const AQParams& p, const Cursor& c, uint32_t sbase, int lane) {
+  using C = InCfg<IN>;
+  const int col0 = c.seg * kSeg;
+  const char* x = static_cast<const char*>(p.x);
+  if (c.row < p.Mi && col0 + kSeg <= p.Ki) {  // interior segment
+    const char* src = x + ((uint64_t)c.row * (uint64_t)p.ldx + (uint32_t)col0) * C::kEs;
 #pragma unroll
-    for (int i = 0; i < kSeg; ++i) v[i] = 0.f;
+    for (int j = 0; j < C::kChunks; ++j) cp_async16(sbase + swz<IN>(j, lane) * 16, src + j * 16, 16u);
     return;
   }
-  if constexpr (IN == MRFP4_DT_F32) {
-    const uint4* p = reinterpret_cast<const uint4*>(static_cast<const float*>(base) + off);
-    uint4 r[8];
+  const int nb = (col0 < p.Ki && c.row < p.Mi) ? (p.Ki - col0) * C::kEs : 0;  // < kSeg * kEs here
+  const char* src = nb ? x + ((uint64_t)c.row * (uint64_t)p.ldx + (uint32_t)col0) * C::kEs : x;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) r[j] = (j < 4 || nvalid == kSeg) ? __ldg(p + j) : make_uint4(0, 0, 0, 0);
+  for (int j = 0; j < C::kChunks; ++j) {
+    const int rem = nb - j * 16;
+    const uint32_t bytes = rem >= 16 ? 16u : (rem > 0 ? (uint32_t)rem : 0u);
+    cp_async16(sbase + swz<IN>(j, lane) * 16, bytes ? src + j * 16 : x, bytes);
+  }
+}
+
+// Shared memory -> P[j] = (v[2j], v[2j+1]), fp32.
+template <int IN>
+__device__ __forceinline__ void load_pairs(uint32_t sbase, int lane, u64 (&P)[kPairs]) {
+  using C = InCfg<IN>;
+  uint32_t w[kSeg * C::kEs / 4];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      v[4 * j + 0] = __uint_as_float(r[j].x);
-      v[4 * j + 1] = __uint_as_float(r[j].y);
-      v[4 * j + 2] = __uint_as_float(r[j].z);
-      v[4 * j + 3] = __uint_as_float(r[j].w);
-    }
-  } else {
-    const uint4* p = reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(base) + off);
-    uint4 r[4];
+  for (int j = 0; j < C::kChunks; ++j) {
+    const uint4 a = lds128(sbase + swz<IN>(j, lane) * 16);
+    w[4 * j] = a.x; w[4 * j + 1] = a.y; w[4 * j + 2] = a.z; w[4 * j + 3] = a.w;
+  }
 #pragma unroll
-    for (int j = 0; j < 4; ++j) r[j] = (j < 2 || nvalid == kSeg) ? __ldg(p + j) : make_uint4(0, 0, 0, 0);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const uint32_t w[4] = {r[j].x, r[j].y, r[j].z, r[j].w};
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        if constexpr (IN == MRFP4_DT_BF16) {
-          bf16x2_to_f32(w[t], v[8 * j + 2 * t], v[8 * j + 2 * t + 1]);
-        } else {
-          __half2 h = *reinterpret_cast<const __half2*>(&w[t]);
-          float2 f = __half22float2(h);
-          v[8 * j + 2 * t] = f.x;
-          v[8 * j + 2 * t + 1] = f.y;
-        }
-      }
+  for (int j = 0; j < kPairs; ++j) {
+    if constexpr (IN == MRFP4_DT_F32) {
+      P[j] = pk(__uint_as_float(w[2 * j]), __uint_as_float(w[2 * j + 1]));
+    } else if constexpr (IN == MRFP4_DT_BF16) {
+      P[j] = pk(__uint_as_float(w[j] << 16), __uint_as_float(w[j] & 0xFFFF0000u));
+    } else {
+      const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[j]));
+      P[j] = pk(f.x, f.y);
     }
   }
 }
 
-// ---------------------------------------------------------------------------
-// fast Walsh-Hadamard transform (unnormalized, Sylvester natural order)
-// ---------------------------------------------------------------------------
+// Unnormalized fast Walsh-Hadamard transform (Sylvester natural order) of the segment.
 template <int HK>
-__device__ __forceinline__ void fwht(float (&v)[kSeg], int lane) {
-  constexpr int kIn = HK < kSeg ? HK : kSeg;
+__device__ __forceinline__ void fwht(u64 (&P)[kPairs], int lane, u64 pm) {
+  // h = 1: (x + y, x - y) inside each pair, one FFMA2 with broadcast x and y
 #pragma unroll
-  for (int h = 1; h < kIn; h <<= 1) {
+  for (int i = 0; i < kPairs; ++i) {
+    const float x = lo_of(P[i]), y = hi_of(P[i]);
+    P[i] = fma2(pk(y, y), pm, pk(x, x));
+  }
+  // h = 2 .. min(k, 32)/2: element h apart = pair h/2 apart
+  constexpr int kIn = (HK < kSeg ? HK : kSeg) / 2;
 #pragma unroll
-    for (int i = 0; i < kSeg; ++i) {
-      if ((i & h) == 0) {
-        const float a = v[i], b = v[i + h];
-        v[i] = a + b;
-        v[i + h] = a - b;
+  for (int hp = 1; hp < kIn; hp <<= 1) {
+#pragma unroll
+    for (int i = 0; i < kPairs; ++i) {
+      if ((i & hp) == 0) {
+        const u64 a = P[i], b = P[i + hp];
+        P[i] = add2(a, b);
+        P[i + hp] = sub2(a, b);
       }
     }
   }
-  // Cross-lane stages: block element index bit 5 (k>=64) lives in lane bit 0,
-  // bit 6 (k=128) in lane bit 1.  Lower partner keeps a+b, upper keeps a-b.
+  // Cross-lane stages: block element index bit 5 (k >= 64) lives in lane bit 0,
+  // bit 6 (k = 128) in lane bit 1.  Lower partner keeps a+b, upper keeps a-b (exact: sg = +-1).
   if constexpr (HK >= 64) {
-    const float sg = (lane & 1) ? -1.f : 1.f;
+    const float s = (lane & 1) ? -1.f : 1.f;
+    const u64 sg = pk(s, s);
 #pragma unroll
-    for (int i = 0; i < kSeg; ++i) {
-      const float p = __shfl_xor_sync(0xffffffffu, v[i], 1);
-      v[i] = fmaf(sg, v[i], p);
-    }
+    for (int i = 0; i < kPairs; ++i) P[i] = fma2(sg, P[i], __shfl_xor_sync(0xffffffffu, P[i], 1));
   }
   if constexpr (HK >= 128) {
-    const float sg = (lane & 2) ? -1.f : 1.f;
+    const float s = (lane & 2) ? -1.f : 1.f;
+    const u64 sg = pk(s, s);
 #pragma unroll
-    for (int i = 0; i < kSeg; ++i) {
-      const float p = __shfl_xor_sync(0xffffffffu, v[i], 2);
-      v[i] = fmaf(sg, v[i], p);
-    }
+    for (int i = 0; i < kPairs; ++i) P[i] = fma2(sg, P[i], __shfl_xor_sync(0xffffffffu, P[i], 2));
   }
 }
 
-// max |v| over [lo, lo+n); NaN/Inf-propagating for rotated data, bit-exact for raw.
-template <int HK, int N>
-__device__ __forceinline__ uint32_t group_absmax_bits(const float (&v)[kSeg], int lo) {
-  if constexpr (HK == 0) {
-    uint32_t m = 0;
+// Absmax of pairs [0, 8) (elements 0..15) and [8, 16) (elements 16..31): NaN-propagating.
+__device__ __forceinline__ void half_amax(const u64 (&P)[kPairs], float& m0, float& m1) {
+  float a[6], b[6];
 #pragma unroll
-    for (int i = 0; i < N; ++i) m = max(m, __float_as_uint(v[lo + i]) & 0x7fffffffu);
-    return m;  // NaN/Inf bit patterns are the largest
-  } else {
-    // After a Hadamard, a non-finite input makes every output of its block
-    // non-finite, so a max seeded with the first element stays non-finite.
-    float m = fabsf(v[lo]);
-#pragma unroll
-    for (int i = 1; i < N; ++i) m = fmaxf(m, fabsf(v[lo + i]));
-    return __float_as_uint(m) & 0x7fffffffu;
+  for (int t = 0; t < 2; ++t) {
+    const int o = 8 * t;
+    float* d = t ? b : a;
+    d[0] = amax3(lo_of(P[o]), hi_of(P[o]), lo_of(P[o + 1]));
+    d[1] = amax3(hi_of(P[o + 1]), lo_of(P[o + 2]), hi_of(P[o + 2]));
+    d[2] = amax3(lo_of(P[o + 3]), hi_of(P[o + 3]), lo_of(P[o + 4]));
+    d[3] = amax3(hi_of(P[o + 4]), lo_of(P[o + 5]), hi_of(P[o + 5]));
+    d[4] = amax3(lo_of(P[o + 6]), hi_of(P[o + 6]), lo_of(P[o + 7]));
+    d[5] = fabsf(hi_of(P[o + 7]));
   }
+  m0 = max3n(max3n(a[0], a[1], a[2]), max3n(a[3], a[4], a[5]), 0.f);
+  m1 = max3n(max3n(b[0], b[1], b[2]), max3n(b[3], b[4], b[5]), 0.f);
 }
 
 // ---------------------------------------------------------------------------
@@ -231,243 +352,358 @@ __device__ __forceinline__ uint32_t cvt_e4m3(float x) {
   return r & 0xFFu;
 }
 
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
 // ---------------------------------------------------------------------------
 // group scale selection
 // ---------------------------------------------------------------------------
 struct GroupScale {
   uint32_t code;
-  float ts;      // tensor scale (f32 value)
   float dec;     // decoded group scale (exact in fp32)
   float f;       // ~ c / (ts * dec), fp32
-  bool slow_all; // force the exact element path (tiny scales)
+  bool slow_all; // force the exact element path (extreme scales)
 };
 
-__device__ __forceinline__ GroupScale mx_group_scale(uint32_t amax_bits, const AQParams& p, float kraw) {
+__device__ __forceinline__ GroupScale mx_group_scale(float amax, const AQParams& p) {
   GroupScale g;
-  int e = 0;
-  if (amax_bits != 0) {
-    const float raw32 = __uint_as_float(amax_bits) * kraw;   // ~ RN64(a/6), <= 1 ulp off
-    const uint32_t rb = __float_as_uint(raw32);
-    const int bexp = (int)(rb >> 23);
-    const int d = (int)(rb & 0x7FFFFFu) - 0x3504F3;          // mantissa of sqrt(2)
-    if (bexp == 0 || bexp == 255 || (d <= 64 && d >= -64)) {
-      e = e8m0_exp_exact(__uint_as_float(amax_bits), p.c64);
-    } else {
-      e = bexp - 127 + (d > 0);
-    }
-    e = min(max(e, -127), 127);
+  const uint32_t ab = __float_as_uint(amax);
+  const uint32_t rb = __float_as_uint(amax * p.kraw);         // ~ RN64(a/6), <= 1 ulp off
+  const int bexp = (int)(rb >> 23);
+  const int d = (int)(rb & 0x7FFFFFu) - 0x3504F3;              // vs the mantissa of sqrt(2)
+  int e = bexp - 127 + (d > 0);
+  if ((uint32_t)(d + 64) <= 128u || bexp == 0 || bexp == 255) {
+    e = ab ? e8m0_exp_exact(amax, p.c64) : 0;                  // rare: near a threshold / extreme
   }
+  e = min(max(e, -127), 127);
   g.code = (uint32_t)(e + 127);
-  g.ts = 1.33333337306976318359375f;                          // f32(4/3), quantizers.py:34,191
-  g.dec = e >= -126 ? __uint_as_float((uint32_t)(e + 127) << 23) : 5.877471754111438e-39f;  // 2^e
-  const float eff = g.ts * g.dec;
-  g.f = p.c32 * __frcp_rn(eff);
-  g.slow_all = e < -100;
+  g.dec = __uint_as_float(e >= -126 ? (uint32_t)(e + 127) << 23 : 0x00400000u);  // 2^e
+  g.slow_all = e < -100 || e > 100;
+  g.f = p.kmx * __uint_as_float((uint32_t)(127 - min(max(e, -100), 100)) << 23);   // c/ts * 2^-e
   return g;
 }
 
-__device__ __forceinline__ GroupScale nv_group_scale(uint32_t amax_bits, const AQParams& p, float kenc,
+__device__ __forceinline__ GroupScale nv_group_scale(float amax, const AQParams& p, float kenc, float knv,
                                                      float st32, double st64, uint32_t zero_code) {
   GroupScale g;
-  uint32_t code;
-  if (amax_bits == 0) {
-    code = zero_code;
-  } else {
-    const float enc32 = __uint_as_float(amax_bits) * kenc;   // ~ RN64(RN64(a/6)/s_T)
-    const uint32_t eb = __float_as_uint(enc32);
-    // E4M3 midpoints have <= 5 significant bits: low 19 mantissa bits are zero.
-    const bool near = ((eb + 64u) & 0x7FFFFu) < 128u;
-    if (near || eb >= 0x7f800000u || eb < 0x38800000u /* < 2^-14 */) {
-      code = e4m3_code_exact(__uint_as_float(amax_bits), p.c64, st64);
-    } else {
-      code = cvt_e4m3(enc32);
-    }
+  const uint32_t ab = __float_as_uint(amax);
+  const float enc32 = amax * kenc;                            // ~ RN64(RN64(a/6)/s_T)
+  const uint32_t eb = __float_as_uint(enc32);
+  uint32_t code = cvt_e4m3(enc32);
+  // E4M3 midpoints have <= 5 significant bits: low 19 mantissa bits are zero.
+  if (((eb + 64u) & 0x7FFFFu) < 128u || eb >= 0x7f800000u || eb < 0x38800000u /* < 2^-14 */) {
+    code = ab ? e4m3_code_exact(amax, p.c64, st64) : zero_code;
   }
   g.code = code;
-  g.ts = st32;
   g.dec = e4m3_value(code);
   const float eff = st32 * g.dec;
-  g.f = eff > 0.f ? p.c32 * __frcp_rn(eff) : 0.f;
-  g.slow_all = eff < 1e-30f;
+  g.slow_all = !(eff >= 1e-30f);
+  g.f = knv * rcp_approx(g.dec);
   return g;
 }
 
-// Quantize 8 consecutive rotated values S[lo..lo+8) against one group scale.
-__device__ __forceinline__ uint32_t quantize8(const float (&v)[kSeg], int lo, const GroupScale& g,
-                                              const AQParams& p) {
+// Codes of the segment as 4 words (word w = elements 8w..8w+7 = pairs 4w..4w+3).
+// s0 scales pairs 0..7 (elements 0..15), s1 pairs 8..15.
+__device__ __forceinline__ void quantize_seg(const u64 (&P)[kPairs], const GroupScale& s0, const GroupScale& s1,
+                                             float ts, const AQParams& p, uint32_t (&w)[4]) {
   constexpr float kEps = 3.814697265625e-06f;  // 2^-18
-  const float fhi = g.f * (1.f + kEps), flo = g.f * (1.f - kEps);
-  float uh[8], ul[8];
+  const float h0 = s0.f * (1.f + kEps), l0 = s0.f * (1.f - kEps);
+  const float h1 = s1.f * (1.f + kEps), l1 = s1.f * (1.f - kEps);
+  uint32_t diff = 0;
 #pragma unroll
-  for (int t = 0; t < 8; ++t) {
-    uh[t] = v[lo + t] * fhi;
-    ul[t] = v[lo + t] * flo;
+  for (int wi = 0; wi < 4; ++wi) {
+    const float fh = wi < 2 ? h0 : h1, fl = wi < 2 ? l0 : l1;
+    float uh[8], ul[8];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const u64 a = mul2(P[4 * wi + t], pk(fh, fh)), b = mul2(P[4 * wi + t], pk(fl, fl));
+      uh[2 * t] = lo_of(a); uh[2 * t + 1] = hi_of(a);
+      ul[2 * t] = lo_of(b); ul[2 * t + 1] = hi_of(b);
+    }
+    const uint32_t a = cvt_e2m1x8(uh), b = cvt_e2m1x8(ul);
+    w[wi] = a;
+    diff |= a ^ b;
   }
-  const uint32_t wh = fix_neg_zero(cvt_e2m1x8(uh));
-  const uint32_t wl = fix_neg_zero(cvt_e2m1x8(ul));
-  uint32_t w = wh;
-  uint32_t diff = wh ^ wl;
-  if (g.slow_all) diff = 0xFFFFFFFFu;
-  if (diff) {
+  if (diff | (uint32_t)(s0.slow_all | s1.slow_all)) {
 #pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      if ((diff >> (4 * t)) & 0xFu) {
-        const uint32_t c = fp4_code_exact(v[lo + t], p.c64, g.ts, g.dec);
-        w = (w & ~(0xFu << (4 * t))) | (c << (4 * t));
+    for (int wi = 0; wi < 4; ++wi) {
+      const GroupScale& g = wi < 2 ? s0 : s1;
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const u64 pr = P[4 * wi + t / 2];
+        const float s = (t & 1) ? hi_of(pr) : lo_of(pr);
+        float a[8], b[8];
+        a[0] = s * (g.f * (1.f + kEps)); b[0] = s * (g.f * (1.f - kEps));
+#pragma unroll
+        for (int z = 1; z < 8; ++z) { a[z] = 0.f; b[z] = 0.f; }
+        if (g.slow_all || ((cvt_e2m1x8(a) ^ cvt_e2m1x8(b)) & 0xFu)) {
+          const uint32_t c = fp4_code_exact(s, p.c64, ts, g.dec);
+          w[wi] = (w[wi] & ~(0xFu << (4 * t))) | (c << (4 * t));
+        }
       }
     }
   }
-  return w;
+#pragma unroll
+  for (int wi = 0; wi < 4; ++wi) w[wi] = fix_neg_zero(w[wi]);
 }
 
 // ---------------------------------------------------------------------------
 // kernels
 // ---------------------------------------------------------------------------
-template <int IN, int HK>
-__device__ __forceinline__ int load_and_rotate(const AQParams& p, int64_t row, int64_t col0,
-                                               float (&v)[kSeg], int lane) {
-  int nvalid = 0;
-  if (row < p.M && col0 < p.K) nvalid = (col0 + kSeg <= p.K) ? kSeg : (int)(p.K - col0);
-  load_seg<IN>(p.x, row * p.ldx + col0, nvalid, v);
-  if constexpr (HK > 0) fwht<HK>(v, lane);
-  return nvalid;
+// Persistent per-lane pipeline over this warp's contiguous item range: issue segment
+// i+2 while segment i is processed.  DIR = -1 walks the range backwards (NVFP4 phase
+// 2 re-reads X; start with what phase 1 left most recently in L2).
+// PDL: EARLY = true issues the first loads before waiting for the predecessor grid
+// (only when X is not produced by it, i.e. NVFP4 phase 2 after phase 1); `ready` runs
+// once after the wait, before the first segment is processed.
+template <int IN, int DIR, bool EARLY, typename R, typename F>
+__device__ __forceinline__ void for_each_seg(const AQParams& p, R&& ready, F&& body) {
+  using C = InCfg<IN>;
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t gw = (int64_t)blockIdx.x * kWarps + warp, tw = (int64_t)gridDim.x * kWarps;
+  const int64_t i0 = gw * p.items / tw, i1 = (gw + 1) * p.items / tw;
+  const int n = (int)(i1 - i0);
+  if constexpr (!EARLY) pdl_wait();
+  if (n <= 0) {
+    if constexpr (EARLY) pdl_wait();
+    ready();
+    return;
+  }
+  const uint32_t base =
+      (uint32_t)__cvta_generic_to_shared(smem_raw) + (uint32_t)((warp * kStages * 32 + lane) * C::kLaneBytes);
+  constexpr uint32_t kStride = 32 * C::kLaneBytes;
+  Cursor ci = cursor_at(p, DIR > 0 ? i0 : i1 - 1, lane), cp = ci;
+#pragma unroll
+  for (int s = 0; s < kStages - 1; ++s) {
+    if (s < n) {
+      issue_seg<IN>(p, ci, base + s * kStride, lane);
+      cursor_step<DIR>(p, ci);
+    }
+    cp_commit();
+  }
+  if constexpr (EARLY) pdl_wait();
+  ready();
+  int rd = 0, wr = kStages - 1;
+  for (int k = 0; k < n; ++k) {
+    if (k + kStages - 1 < n) {
+      issue_seg<IN>(p, ci, base + wr * kStride, lane);
+      cursor_step<DIR>(p, ci);
+    }
+    cp_commit();
+    cp_wait<kStages - 1>();
+    body(cp, base + rd * kStride);
+    cursor_step<DIR>(p, cp);
+    rd = rd + 1 == kStages ? 0 : rd + 1;
+    wr = wr + 1 == kStages ? 0 : wr + 1;
+  }
+  cp_wait<0>();
 }
 
 // NVFP4 phase 1: max |S| over the whole tensor (quantizers.py:198-200 needs it first).
 template <int IN, int HK>
-__global__ void __launch_bounds__(kThreads) k_tensor_absmax(AQParams p) {
-  const int tid = threadIdx.x, lane = tid & 31;
-  const int64_t row = (int64_t)blockIdx.y * kRowsPerCta + (tid >> 2);
-  const int64_t col0 = ((int64_t)blockIdx.x * kSegsPerRow + (tid & 3)) * kSeg;
-  float v[kSeg];
-  const int nvalid = load_and_rotate<IN, HK>(p, row, col0, v, lane);
-  uint32_t m = 0;
-  if (nvalid) m = group_absmax_bits<HK, kSeg>(v, 0);  // zero-padded half segments are harmless
-  m = __reduce_max_sync(0xffffffffu, m);
-  __shared__ uint32_t smax[kThreads / 32];
-  if (lane == 0) smax[tid >> 5] = m;
+__global__ void __launch_bounds__(kThreads, 4) k_tensor_absmax(AQParams p) {
+  const int lane = threadIdx.x & 31;
+  pdl_trigger();
+  float m = 0.f;
+  for_each_seg<IN, 1, false>(p, [] {}, [&](const Cursor&, uint32_t sbase) {
+    u64 P[kPairs];
+    load_pairs<IN>(sbase, lane, P);
+    if constexpr (HK > 0) fwht<HK>(P, lane, p.pm);
+    float a, b;
+    half_amax(P, a, b);   // padding rows / columns were zero-filled
+    m = max3n(a, b, m);
+  });
+  uint32_t mb = __float_as_uint(m);
+  mb = mb > 0x7f800000u ? 0x7fc00000u : mb;  // canonical NaN
+  mb = __reduce_max_sync(0xffffffffu, mb);
+  __shared__ uint32_t smax[kWarps];
+  if (lane == 0) smax[threadIdx.x >> 5] = mb;
   __syncthreads();
-  if (tid < 32) {
-    uint32_t x = tid < kThreads / 32 ? smax[tid] : 0u;
+  if (threadIdx.x < 32) {
+    uint32_t x = threadIdx.x < kWarps ? smax[threadIdx.x] : 0u;
     x = __reduce_max_sync(0xffffffffu, x);
-    if (tid == 0 && x) {
-      atomicMax(p.gmax, min(x, 0x7fc00000u));
+    if (threadIdx.x == 0 && x) {
+      atomicMax(p.gmax, x);
       if (x >= 0x7f800000u) atomic_or_status(p.status, MRFP4_STATUS_NONFINITE);
+    }
+  }
+}
+
+// sf_offset in 32-bit arithmetic (scale buffers are < 4 GiB).
+__device__ __forceinline__ uint32_t sf_off32(uint32_t r, uint32_t c, uint32_t cb) {
+  return ((r >> 7) * cb + (c >> 2)) * 512u + (r & 31u) * 16u + ((r >> 5) & 3u) * 4u + (c & 3u);
+}
+
+// Zero the padding of the swizzled scale buffer: rows [M, rows_pad) (whole 4-byte words)
+// and columns [sf_cols, 4*col_blocks) of the real rows (<= 3 bytes per row).
+__device__ __forceinline__ void zero_sf_padding(const AQParams& p) {
+  const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
+  const uint32_t M = (uint32_t)p.Mi, cb = p.cb;
+  const uint32_t n_words = ((uint32_t)p.rows_pad - M) * cb;
+  for (uint32_t i = tid; i < n_words; i += nth) {
+    const uint32_t r = M + i / cb, blk = i - (i / cb) * cb;
+    *reinterpret_cast<uint32_t*>(p.sf + sf_off32(r, 4 * blk, cb)) = 0u;
+  }
+  const uint32_t sfc = (uint32_t)p.sf_cols, extra = 4 * cb - sfc;
+  if (extra) {
+    for (uint32_t i = tid; i < M * extra; i += nth) {
+      const uint32_t r = i / extra;
+      p.sf[sf_off32(r, sfc + (i - r * extra), cb)] = 0;
     }
   }
 }
 
 template <int IN, int FMT, int HK>
 __global__ void __launch_bounds__(kThreads, 3) k_act_quant(AQParams p) {
-  constexpr int G = FMT == MRFP4_FMT_MXFP4 ? 32 : 16;
-  constexpr int NG = kSeg / G;
-  const int tid = threadIdx.x, lane = tid & 31;
-  const int64_t row = (int64_t)blockIdx.y * kRowsPerCta + (tid >> 2);
-  const int64_t seg = (int64_t)blockIdx.x * kSegsPerRow + (tid & 3);
-  const int64_t col0 = seg * kSeg;
+  const int lane = threadIdx.x & 31;
 
-  // Per-launch constants (uniform).
-  float kscale;          // MXFP4: ~c/6 ; NVFP4: ~c/6/s_T
-  float st32 = 1.f;
+  pdl_trigger();
+  // Per-launch constants (uniform); NVFP4's depend on phase 1 (read after the PDL wait).
+  float st32 = 1.33333337306976318359375f;   // MXFP4 tensor scale f32(4/3), quantizers.py:34,191
   double st64 = 1.0;
+  float kenc = 0.f, knv = 0.f;
   uint32_t zero_code = 0;
+  auto ready = [&] {
+    if constexpr (FMT == MRFP4_FMT_NVFP4) {
+      const float smax = __uint_as_float(*(volatile uint32_t*)p.gmax);  // max |S| over the tensor
+      const double top = (double)smax * p.c64 / 6.0;      // absmax.max() / FP4_MAX
+      st32 = top > 0.0 ? __double2float_rn(top / 448.0) : 1.0f;  // f32(top / E4M3 max)
+      st64 = (double)st32;
+      zero_code = e4m3_rne64(1.0 / st64);                  // raw = 1.0 sentinel (quantizers.py:187)
+      kenc = __double2float_rn(p.c64 / 6.0 / st64);
+      knv = __double2float_rn(p.c64 / st64);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) *p.tensor_scale = st32;
+  };
+
+  uint32_t bad = 0;
+  for_each_seg<IN, FMT == MRFP4_FMT_NVFP4 ? -1 : 1, FMT == MRFP4_FMT_NVFP4>(p, ready, [&](const Cursor& c, uint32_t sbase) {
+    u64 P[kPairs];
+    load_pairs<IN>(sbase, lane, P);
+    if constexpr (HK > 0) fwht<HK>(P, lane, p.pm);
+    const int col0 = c.seg * kSeg;
+    if (col0 >= p.Ki || c.row >= p.Mi) return;           // idle lane (after the shuffles)
+    const bool full = col0 + kSeg <= p.Ki;                // else a 16-element tail (K % 32 == 16)
+
+    float a0, a1;
+    half_amax(P, a0, a1);
+    GroupScale s0, s1;
+    uint32_t sfc;
+    if constexpr (FMT == MRFP4_FMT_NVFP4) {
+      s0 = nv_group_scale(a0, p, kenc, knv, st32, st64, zero_code);
+      s1 = nv_group_scale(a1, p, kenc, knv, st32, st64, zero_code);
+      if (__float_as_uint(a0) >= 0x7f800000u || (full && __float_as_uint(a1) >= 0x7f800000u))
+        bad |= MRFP4_STATUS_NONFINITE;
+      if (s0.code == 0 || (full && s1.code == 0)) bad |= MRFP4_STATUS_SCALE_UNDERFLOW;
+      sfc = s0.code | (full ? s1.code << 8 : 0u);
+    } else {
+      const float a = max3n(a0, a1, 0.f);
+      if (__float_as_uint(a) >= 0x7f800000u) bad |= MRFP4_STATUS_NONFINITE;
+      s0 = mx_group_scale(a, p);
+      s1 = s0;
+      sfc = s0.code;
+    }
+    uint32_t w[4];
+    quantize_seg(P, s0, s1, st32, p, w);
+
+    uint8_t* cdst = p.codes + (uint64_t)c.row * p.half_k + (uint32_t)(col0 >> 1);
+    if (full) {
+      if ((p.Ki & 31) == 0) {
+        *reinterpret_cast<uint4*>(cdst) = make_uint4(w[0], w[1], w[2], w[3]);
+      } else {
+        reinterpret_cast<uint2*>(cdst)[0] = make_uint2(w[0], w[1]);
+        reinterpret_cast<uint2*>(cdst)[1] = make_uint2(w[2], w[3]);
+      }
+    } else {
+      *reinterpret_cast<uint2*>(cdst) = make_uint2(w[0], w[1]);
+    }
+    if constexpr (FMT == MRFP4_FMT_MXFP4) {
+      p.sf[sf_off32(c.row, c.seg, p.cb)] = (uint8_t)sfc;
+    } else {
+      // columns 2*seg, 2*seg+1 share a 16-bit word of the swizzled layout
+      *reinterpret_cast<uint16_t*>(p.sf + sf_off32(c.row, 2 * c.seg, p.cb)) = (uint16_t)sfc;
+    }
+  });
+  if (bad) atomic_or_status(p.status, bad);
+  zero_sf_padding(p);
   if constexpr (FMT == MRFP4_FMT_NVFP4) {
-    const float smax = __uint_as_float(*p.gmax);         // max |S| over the tensor
-    const double top = (double)smax * p.c64 / 6.0;      // absmax.max() / FP4_MAX
-    st32 = top > 0.0 ? __double2float_rn(top / 448.0) : 1.0f;  // f32(top / E4M3 max)
-    st64 = (double)st32;
-    zero_code = e4m3_rne64(1.0 / st64);                  // raw = 1.0 sentinel (quantizers.py:187)
-    kscale = __double2float_rn(p.c64 / 6.0 / st64);
-    if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) *p.tensor_scale = st32;
-  } else {
-    kscale = __double2float_rn(p.c64 / 6.0);
-    if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) *p.tensor_scale = 1.33333337306976318359375f;
-  }
-
-  float v[kSeg];
-  const int nvalid = load_and_rotate<IN, HK>(p, row, col0, v, lane);
-
-  const bool row_in_pad = row < p.rows_pad;
-  if (nvalid == 0) {
-    // Zero the padding of the swizzled scale buffer (rows >= M, columns >= K/G).
-    if (row_in_pad) {
-#pragma unroll
-      for (int g = 0; g < NG; ++g) {
-        const int64_t c = seg * NG + g;
-        if (c < p.sf_col_blocks * 4) p.sf[sf_offset(row, c, p.sf_col_blocks)] = 0;
+    // Last CTA out re-arms the workspace (gmax = 0, counter = 0) for the next call:
+    // every CTA read gmax before it arrives here.
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      if (atomicAdd(p.gmax + 1, 1u) == gridDim.x - 1) {
+        p.gmax[0] = 0u;
+        p.gmax[1] = 0u;
+        __threadfence();
       }
     }
-    return;
   }
+}
 
-  uint32_t words[kSeg / 8];
-  uint32_t sfc[NG];
-  uint32_t bad = 0;
-#pragma unroll
-  for (int g = 0; g < NG; ++g) {
-    const uint32_t ab = group_absmax_bits<HK, G>(v, g * G);
-    const bool real = g * G < nvalid;  // a trailing half segment pads group 1 with zeros
-    if (real && ab >= 0x7f800000u) bad |= MRFP4_STATUS_NONFINITE;
-    GroupScale gs;
-    if constexpr (FMT == MRFP4_FMT_NVFP4) {
-      gs = nv_group_scale(ab, p, kscale, st32, st64, zero_code);
-      if (real && gs.code == 0) bad |= MRFP4_STATUS_SCALE_UNDERFLOW;
-    } else {
-      gs = mx_group_scale(ab, p, kscale);
-    }
-    sfc[g] = gs.code;
-#pragma unroll
-    for (int j = 0; j < G / 8; ++j) words[g * (G / 8) + j] = quantize8(v, g * G + 8 * j, gs, p);
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
   }
-  if (bad) atomic_or_status(p.status, bad);
+  return n;
+}
 
-  // codes: 16 bytes (or 8 for a trailing half segment) at codes[row, col0/2]
-  uint8_t* cdst = p.codes + row * (p.K >> 1) + (col0 >> 1);
-  if (nvalid == kSeg) {
-    if ((p.K & 31) == 0) {
-      *reinterpret_cast<uint4*>(cdst) = make_uint4(words[0], words[1], words[2], words[3]);
-    } else {
-      reinterpret_cast<uint2*>(cdst)[0] = make_uint2(words[0], words[1]);
-      reinterpret_cast<uint2*>(cdst)[1] = make_uint2(words[2], words[3]);
-    }
-  } else {
-    *reinterpret_cast<uint2*>(cdst) = make_uint2(words[0], words[1]);
+// One CTA set per SM that the occupancy calculator allows (cached per kernel).
+template <auto Kern>
+int launch_persistent(int smem, const AQParams& p, cudaStream_t s) {
+  static std::once_flag once;
+  static int per_sm = -1;
+  std::call_once(once, [&] {
+    int n = 0;
+    // Max-shared carveout (the GEMM's too), so K1 -> K2 -> K1 never reconfigures L1/SMEM.
+    cudaFuncSetAttribute(Kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    if (cudaFuncSetAttribute(Kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) == cudaSuccess &&
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, Kern, kThreads, smem) == cudaSuccess)
+      per_sm = std::max(n, 1);
+  });
+  if (per_sm < 0) return MRFP4_ECUDA;
+  const int64_t need = ceil_div(p.items, kWarps);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)per_sm * num_sms()));
+  return launch_pdl(Kern, dim3(grid), dim3(kThreads), smem, s, p) == cudaSuccess ? MRFP4_OK : MRFP4_ECUDA;
+}
+
+template <int IN, int FMT, int HK>
+int launch_hk(const AQParams& p, cudaStream_t s) {
+  constexpr int smem = InCfg<IN>::kSmem;
+  if constexpr (FMT == MRFP4_FMT_NVFP4) {
+    const int rc = launch_persistent<k_tensor_absmax<IN, HK>>(smem, p, s);
+    if (rc != MRFP4_OK) return rc;
   }
-  // scale codes straight into the swizzled layout
-  if constexpr (NG == 1) {
-    p.sf[sf_offset(row, seg, p.sf_col_blocks)] = (uint8_t)sfc[0];
-  } else {
-    const int64_t c0 = seg * 2;                  // c0 even -> c0, c0+1 share a 16-bit word
-    const uint32_t hi = (nvalid == kSeg) ? sfc[1] : 0u;
-    *reinterpret_cast<uint16_t*>(p.sf + sf_offset(row, c0, p.sf_col_blocks)) =
-        (uint16_t)(sfc[0] | (hi << 8));
-  }
+  return launch_persistent<k_act_quant<IN, FMT, HK>>(smem, p, s);
 }
 
 template <int IN, int FMT>
-int dispatch_hk(const AQParams& p, int hk, dim3 grid, cudaStream_t s) {
+int dispatch_hk(const AQParams& p, int hk, cudaStream_t s) {
   switch (hk) {
-#define MRFP4_CASE(K)                                                            \
-  case K:                                                                        \
-    if (FMT == MRFP4_FMT_NVFP4) k_tensor_absmax<IN, K><<<grid, kThreads, 0, s>>>(p); \
-    k_act_quant<IN, FMT, K><<<grid, kThreads, 0, s>>>(p);                        \
-    break;
-    MRFP4_CASE(0)
-    MRFP4_CASE(16)
-    MRFP4_CASE(32)
-    MRFP4_CASE(64)
-    MRFP4_CASE(128)
-#undef MRFP4_CASE
-    default:
-      return MRFP4_EUNSUPPORTED;
+    case 0: return launch_hk<IN, FMT, 0>(p, s);
+    case 16: return launch_hk<IN, FMT, 16>(p, s);
+    case 32: return launch_hk<IN, FMT, 32>(p, s);
+    case 64: return launch_hk<IN, FMT, 64>(p, s);
+    case 128: return launch_hk<IN, FMT, 128>(p, s);
+    default: return MRFP4_EUNSUPPORTED;
   }
-  return MRFP4_OK;
 }
 
 template <int IN>
-int dispatch_fmt(const AQParams& p, int fmt, int hk, dim3 grid, cudaStream_t s) {
-  return fmt == MRFP4_FMT_MXFP4 ? dispatch_hk<IN, MRFP4_FMT_MXFP4>(p, hk, grid, s)
-                                : dispatch_hk<IN, MRFP4_FMT_NVFP4>(p, hk, grid, s);
+int dispatch_fmt(const AQParams& p, int fmt, int hk, cudaStream_t s) {
+  return fmt == MRFP4_FMT_MXFP4 ? dispatch_hk<IN, MRFP4_FMT_MXFP4>(p, hk, s)
+                                : dispatch_hk<IN, MRFP4_FMT_NVFP4>(p, hk, s);
 }
 
 }  // namespace
@@ -490,19 +726,31 @@ int launch_act_quant(const void* x, int x_dtype, int64_t M, int64_t K, int64_t l
   p.sf_cols = K / G;
   p.sf_col_blocks = ceil_div(p.sf_cols, 4);
   p.rows_pad = ceil_div(M, 128) * 128;
-  p.c64 = hk ? 1.0 / sqrt((double)hk) : 1.0;
-  p.c32 = (float)p.c64;
-  // Columns: enough segments to cover K and the padded scale columns.
-  const int64_t segs = std::max(ceil_div(K, kSeg), ceil_div(p.sf_col_blocks * 4, kSeg / G));
-  dim3 grid((unsigned)ceil_div(segs, kSegsPerRow), (unsigned)ceil_div(p.rows_pad, kRowsPerCta));
-  if (fmt == MRFP4_FMT_NVFP4) {
-    if (cudaMemsetAsync(p.gmax, 0, sizeof(uint32_t), s) != cudaSuccess) return MRFP4_ECUDA;
+  const int64_t nseg = ceil_div(K, kSeg);
+  int lb = 0;
+  while ((1 << lb) < nseg && lb < 5) ++lb;
+  if (hk >= 128) lb = std::max(lb, 2);  // a 128-element block spans 4 lanes
+  else if (hk >= 64) lb = std::max(lb, 1);
+  p.lane_bits = lb;
+  p.nchunk = (int)ceil_div(nseg, 1 << lb);
+  p.seg_span = p.nchunk << lb;
+  p.items = ceil_div(M, 32 >> lb) * p.nchunk;
+  p.Mi = (int)M;
+  p.Ki = (int)K;
+  p.half_k = (uint32_t)(K / 2);
+  p.cb = (uint32_t)p.sf_col_blocks;
+  {
+    const float pm[2] = {1.f, -1.f};
+    memcpy(&p.pm, pm, sizeof(pm));
   }
+  p.c64 = hk ? 1.0 / sqrt((double)hk) : 1.0;
+  p.kraw = (float)(p.c64 / 6.0);
+  p.kmx = (float)(p.c64 / (double)1.33333337306976318359375f);
   int rc;
   switch (x_dtype) {
-    case MRFP4_DT_BF16: rc = dispatch_fmt<MRFP4_DT_BF16>(p, fmt, hk, grid, s); break;
-    case MRFP4_DT_F16: rc = dispatch_fmt<MRFP4_DT_F16>(p, fmt, hk, grid, s); break;
-    case MRFP4_DT_F32: rc = dispatch_fmt<MRFP4_DT_F32>(p, fmt, hk, grid, s); break;
+    case MRFP4_DT_BF16: rc = dispatch_fmt<MRFP4_DT_BF16>(p, fmt, hk, s); break;
+    case MRFP4_DT_F16: rc = dispatch_fmt<MRFP4_DT_F16>(p, fmt, hk, s); break;
+    case MRFP4_DT_F32: rc = dispatch_fmt<MRFP4_DT_F32>(p, fmt, hk, s); break;
     default: return MRFP4_EUNSUPPORTED;
   }
   if (rc != MRFP4_OK) return rc;

@@ -3,6 +3,7 @@
 // (/root/reference/pkg/src/microfp/quantizers.py:95-111) and returns a status;
 // kernels report data errors through the caller's device status word.
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <string>
 
@@ -18,6 +19,16 @@ int launch_sf_swizzle(const uint8_t* src, uint8_t* dst, int64_t rows, int64_t co
 int launch_sf_unswizzle(const uint8_t* src, uint8_t* dst, int64_t rows, int64_t cols, cudaStream_t s);
 int launch_dequantize(const uint8_t* codes, const uint8_t* sf, const float* ts, int64_t rows, int64_t cols, int fmt,
                       float* out, cudaStream_t s);
+}  // namespace mrfp4
+
+namespace mrfp4 {
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("MRFP4_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 }  // namespace mrfp4
 
 namespace {
@@ -71,6 +82,8 @@ int mrfp4_act_quant(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ld
   const int es = elt_size(x_dtype);
   if (es == 0) return fail(MRFP4_EUNSUPPORTED, "unsupported input dtype %d", x_dtype);
   if (M < 1 || K < 1) return fail(MRFP4_EINVAL, "expected a non-empty 2-D matrix");  // quantizers.py:97-98
+  if (M > INT32_MAX / 2 || K > INT32_MAX / 2 || (M * K) / 32 > (int64_t)UINT32_MAX)
+    return fail(MRFP4_EUNSUPPORTED, "matrix too large for one call (split the rows)");
   if (K % G) return fail(MRFP4_EINVAL, "columns (%lld) not divisible by group size (%d)", (long long)K, G);
   if (had_k != 0 && had_k != 16 && had_k != 32 && had_k != 64 && had_k != 128)
     return fail(MRFP4_EUNSUPPORTED, "unsupported Hadamard block %d (GPU path: 16, 32, 64, 128)", had_k);
@@ -81,8 +94,8 @@ int mrfp4_act_quant(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ld
   if (((uint64_t)ldx * es) % 16 || !aligned(x, 16))
     return fail(MRFP4_EUNSUPPORTED, "input rows must be 16-byte aligned");
   if (!aligned(codes, 16) || !aligned(sf, 2)) return fail(MRFP4_EUNSUPPORTED, "output buffers must be 16-byte aligned");
-  if (fmt == MRFP4_FMT_NVFP4 && (workspace == nullptr || workspace_bytes < 4))
-    return fail(MRFP4_EINVAL, "NVFP4 needs a >= 4-byte device workspace");
+  if (fmt == MRFP4_FMT_NVFP4 && (workspace == nullptr || workspace_bytes < 8 || !aligned(workspace, 4)))
+    return fail(MRFP4_EINVAL, "NVFP4 needs an 8-byte, 4-byte aligned, zero-initialised device workspace");
   const int rc = mrfp4::launch_act_quant(x, x_dtype, M, K, ldx, fmt, had_k, codes, sf, tensor_scale, status,
                                          workspace, static_cast<cudaStream_t>(stream));
   return cuda_status(rc, "mrfp4_act_quant");

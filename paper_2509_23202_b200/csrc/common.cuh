@@ -1,6 +1,7 @@
 // Shared helpers for the mrfp4 sm_100a kernels (B200).
 #pragma once
 #include <cstdint>
+#include <utility>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -30,6 +31,32 @@ __device__ __forceinline__ float e4m3_value(uint32_t code) {
 
 __device__ __forceinline__ void atomic_or_status(uint32_t* status, uint32_t bits) {
   if (status) atomicOr(status, bits);
+}
+
+// Programmatic dependent launch (PDL).  Every kernel is launched with programmatic
+// stream serialization, so it may start while its predecessor in the stream is still
+// running: pdl_wait() blocks until the predecessor grid has completed and its writes
+// are visible, and MUST precede any read of data a predecessor may produce.
+// pdl_trigger() lets the successor's CTAs launch (they still wait in pdl_wait()).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// Launch `kern` on `s` with the PDL attribute (disabled when MRFP4_PDL=0 in the environment).
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
 }  // namespace mrfp4

@@ -191,12 +191,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  pdl_trigger();
 
   const int num_tiles = g.num_m_blk * g.num_n_blk;
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
     if (lane == 0) {
+      pdl_wait();  // A, its scale factors and tensor scale come from the act-quant kernel
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
@@ -275,6 +277,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {
     // ------------------------------------------------------------ epilogue
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    pdl_wait();
     const float alpha = __ldg(g.a_ts) * __ldg(g.b_ts);
     uint32_t acc_phase = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
@@ -384,10 +387,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
   sm100::cluster_sync();
   sm100::tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  pdl_trigger();
 
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------------------- producer
+      pdl_wait();  // A, its scale factors and tensor scale come from the act-quant kernel
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = cluster; tile < num_tiles; tile += nclusters) {
@@ -523,6 +528,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
   } else {
     // ------------------------------------------------------ epilogue (both CTAs)
     const int q = warp & 3;
+    pdl_wait();
     const float alpha = __ldg(g.a_ts) * __ldg(g.b_ts);
     uint32_t acc_phase = 0;
     for (int tile = cluster; tile < num_tiles; tile += nclusters) {
@@ -635,8 +641,9 @@ int launch(const uint8_t* a, const uint8_t* b, const GemmArgs& args0, cudaStream
   const int tiles = g.num_m_blk * g.num_n_blk;
   int grid = std::min(tiles, num_sms());
   if (g_force_grid > 0) grid = std::min(grid, g_force_grid);
-  k_gemm_fp4<VEC, BN, OUT><<<grid, kThreads, C::kSmem, s>>>(tmA, tmB, g);
-  return cudaPeekAtLastError() == cudaSuccess ? MRFP4_OK : MRFP4_ECUDA;
+  return launch_pdl(k_gemm_fp4<VEC, BN, OUT>, dim3(grid), dim3(kThreads), C::kSmem, s, tmA, tmB, g) == cudaSuccess
+             ? MRFP4_OK
+             : MRFP4_ECUDA;
 }
 
 template <int VEC, int OUT>
@@ -666,8 +673,10 @@ int launch2(const uint8_t* a, const uint8_t* b, const GemmArgs& args0, cudaStrea
   const int clusters = std::min(tiles, num_sms() / 2);
   int nclu = clusters;
   if (g_force_grid > 0) nclu = std::min(nclu, std::max(1, g_force_grid / 2));
-  k_gemm_fp4_2sm<VEC, OUT><<<2 * nclu, C::kThreads2, C::kSmem, s>>>(tmA, tmB, tmSFA, tmSFB, g);
-  return cudaPeekAtLastError() == cudaSuccess ? MRFP4_OK : MRFP4_ECUDA;
+  return launch_pdl(k_gemm_fp4_2sm<VEC, OUT>, dim3(2 * nclu), dim3(C::kThreads2), C::kSmem, s, tmA, tmB, tmSFA,
+                    tmSFB, g) == cudaSuccess
+             ? MRFP4_OK
+             : MRFP4_ECUDA;
 }
 
 }  // namespace

@@ -143,7 +143,9 @@ def test_input_dtypes(dtype):
 
 @pytest.mark.parametrize("M,K,fmt,k", [
     (1, 32, "mxfp4", 0), (1, 16, "nvfp4", 16), (3, 48, "nvfp4", 16), (129, 96, "mxfp4", 32),
-    (130, 80, "nvfp4", 0), (257, 384, "nvfp4", 128), (127, 640, "mxfp4", 64), (5, 4096, "nvfp4", 128)])
+    (130, 80, "nvfp4", 0), (257, 384, "nvfp4", 128), (127, 640, "mxfp4", 64), (5, 4096, "nvfp4", 128),
+    (2, 1056, "mxfp4", 32), (7, 2080, "nvfp4", 16), (9, 1040, "nvfp4", 0), (33, 4112, "nvfp4", 16),
+    (300, 3200, "mxfp4", 128), (65, 1536, "nvfp4", 64)])
 def test_ragged_shapes(M, K, fmt, k):
     rng = np.random.default_rng(M * 7 + K)
     X = O.bf16_round(rng.standard_normal((M, K)))
@@ -184,3 +186,28 @@ def test_numpy_input_accepted():
     gpu = P.quantize_rtn(X, SPEC["mxfp4"])
     code_rate, scale_rate, ts = _match(gpu, ora)
     assert code_rate == 1.0 and scale_rate == 1.0 and ts == ora.tensor_scale
+
+
+def test_strided_rows():
+    """Row stride ldx > K (a column slice of a wider activation) goes through the C-ABI as-is."""
+    rng = np.random.default_rng(5)
+    X = O.bf16_round(rng.standard_normal((96, 1024 + 64)))
+    full = _gpu(X)
+    view = full[:, :1024]
+    assert view.stride(0) == 1024 + 64
+    for fmt, k in (("mxfp4", 32), ("nvfp4", 16)):
+        ora = O.quantize_rtn(X[:, :1024], fmt, hadamard=k)
+        code_rate, scale_rate, ts = _match(P.quantize_rtn(view, SPEC[fmt], transform=_tr(k)), ora)
+        assert code_rate == 1.0 and scale_rate == 1.0 and ts == ora.tensor_scale
+
+
+@pytest.mark.parametrize("fmt,k", [("mxfp4", 16), ("mxfp4", 0), ("nvfp4", 0), ("nvfp4", 16), ("mxfp4", 128)])
+@pytest.mark.parametrize("bad", [float("nan"), float("inf")])
+def test_nonfinite_anywhere_in_group_raises(fmt, k, bad):
+    """quantizers.py:99-100: any non-finite element is a DataError -- including one in the
+    second Hadamard block of a 32-wide MXFP4 group (H16 < G) and in the odd row of a pair."""
+    for r, c in ((0, 0), (1, 31), (3, 17), (2, 1000)):
+        X = np.ones((5, 1024), dtype=np.float32)
+        X[r, c] = bad
+        with pytest.raises(P.DataError):
+            P.quantize_rtn(_gpu(X), SPEC[fmt], transform=_tr(k))
