@@ -20,6 +20,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstring>
 #include <mutex>
 
 #include "common.cuh"
@@ -75,57 +76,72 @@ struct GemmArgs {
 
 
 
-// Issue the NK tcgen05.mma of one k-block (compile-time count: no runtime control flow
-// in the issue path -- a data-dependent loop bound here measurably slows issue).
-template <int VEC, int NK, int M, int N, int kNB, bool PAIR>
-__device__ __forceinline__ void issue_kblock(uint32_t d_tmem, uint32_t a_s, uint32_t b_s, uint32_t sfa_t, uint32_t sfb_t,
-                                             bool first) {
+// Advance a shared-memory descriptor's start-address field (bits [0,14), address >> 4)
+// by `x` 16-byte units.  No carry can leave the field (SMEM < 228 KB), so only the low
+// word changes: one IADD instead of re-encoding the descriptor.
+__device__ __forceinline__ uint64_t desc_add(uint64_t d, uint32_t x) {
+  uint64_t r;
+  asm("{\n\t.reg .b32 lo, hi;\n\tmov.b64 {lo, hi}, %1;\n\tadd.u32 lo, lo, %2;\n\tmov.b64 %0, {lo, hi};\n\t}"
+      : "=l"(r)
+      : "l"(d), "r"(x));
+  return r;
+}
+
+// Issue MMAs k in [K0, K1) of one k-block.  The issuing thread's per-MMA work is kept
+// to a few integer adds on precomputed stage descriptors: with the descriptors
+// re-encoded per MMA the single issuing thread (dependent uniform-datapath chains)
+// could not keep up with the tensor pipe (measured ~170-200 vs 128 cycles per MMA).
+//   ad, bd   SMEM descriptors of this stage's A / B tiles at k = 0
+//   sfa, sfb TMEM column of this stage's scale-factor slots
+template <int VEC, int K0, int K1, int M, int N, int kNB, bool PAIR>
+__device__ __forceinline__ void issue_mmas(uint32_t d_tmem, uint64_t ad, uint64_t bd, uint32_t sfa, uint32_t sfb,
+                                           bool first) {
 #pragma unroll
-  for (int k = 0; k < NK; ++k) {
-    const int atom = VEC == 16 ? k : (k >> 1);
+  for (int k = K0; k < K1; ++k) {
+    constexpr int kStepDesc = (UMMA_K / 2) >> 4;  // 32 B of K per MMA
+    const uint32_t atom = VEC == 16 ? k : (k >> 1);
     const uint32_t sfid = VEC == 16 ? 0u : (uint32_t)(k & 1) * 2u;
-    const uint64_t adesc = sm100::smem_desc(a_s + k * (UMMA_K / 2), 16, 1024, 2);
-    const uint64_t bdesc = sm100::smem_desc(b_s + k * (UMMA_K / 2), 16, 1024, 2);
     const uint32_t idesc = sm100::idesc_fp4(M, N, VEC == 32, sfid, sfid);
-    const uint32_t acc = (first && k == 0) ? 0u : 1u;
+    const uint32_t acc = (K0 == 0 && k == 0 && first) ? 0u : 1u;
+    const uint64_t adk = desc_add(ad, k * kStepDesc), bdk = desc_add(bd, k * kStepDesc);
+    const uint32_t sa = sfa + (atom * 4 + (sfid << 30)), sb = sfb + (atom * kNB * 4 + (sfid << 30));
     if constexpr (PAIR)
-      sm100::tc_mma_fp4_2sm<VEC>(d_tmem, adesc, bdesc, idesc, (sfa_t + atom * 4) | (sfid << 30),
-                                 (sfb_t + atom * kNB * 4) | (sfid << 30), acc);
+      sm100::tc_mma_fp4_2sm<VEC>(d_tmem, adk, bdk, idesc, sa, sb, acc);
     else
-      sm100::tc_mma_fp4<VEC>(d_tmem, adesc, bdesc, idesc, (sfa_t + atom * 4) | (sfid << 30),
-                             (sfb_t + atom * kNB * 4) | (sfid << 30), acc);
+      sm100::tc_mma_fp4<VEC>(d_tmem, adk, bdk, idesc, sa, sb, acc);
   }
 }
 
-// MMAs k in [K0, K1) of a k-block (K0 > 0: always accumulate).
-template <int VEC, int K0, int K1, int M, int N, int kNB, bool PAIR>
-__device__ __forceinline__ void issue_kblock_from(uint32_t d_tmem, uint32_t a_s, uint32_t b_s, uint32_t sfa_t,
-                                                  uint32_t sfb_t, bool first) {
+// Warp-converged 2-CTA variant: all lanes run it, lane `el` issues.
+template <int VEC, int K0, int K1, int M, int N, int kNB>
+__device__ __forceinline__ void issue_mmas_warp(uint32_t el, uint32_t d_tmem, uint64_t ad, uint64_t bd, uint32_t sfa,
+                                                uint32_t sfb, bool first) {
 #pragma unroll
   for (int k = K0; k < K1; ++k) {
-    const int atom = VEC == 16 ? k : (k >> 1);
+    constexpr int kStepDesc = (UMMA_K / 2) >> 4;
+    const uint32_t atom = VEC == 16 ? k : (k >> 1);
     const uint32_t sfid = VEC == 16 ? 0u : (uint32_t)(k & 1) * 2u;
-    const uint64_t adesc = sm100::smem_desc(a_s + k * (UMMA_K / 2), 16, 1024, 2);
-    const uint64_t bdesc = sm100::smem_desc(b_s + k * (UMMA_K / 2), 16, 1024, 2);
     const uint32_t idesc = sm100::idesc_fp4(M, N, VEC == 32, sfid, sfid);
-    const uint32_t acc = (first && k == 0) ? 0u : 1u;
-    if constexpr (PAIR)
-      sm100::tc_mma_fp4_2sm<VEC>(d_tmem, adesc, bdesc, idesc, (sfa_t + atom * 4) | (sfid << 30),
-                                 (sfb_t + atom * kNB * 4) | (sfid << 30), acc);
-    else
-      sm100::tc_mma_fp4<VEC>(d_tmem, adesc, bdesc, idesc, (sfa_t + atom * 4) | (sfid << 30),
-                             (sfb_t + atom * kNB * 4) | (sfid << 30), acc);
+    const uint32_t acc = (K0 == 0 && k == 0 && first) ? 0u : 1u;
+    sm100::tc_mma_fp4_2sm_if<VEC>(el, d_tmem, desc_add(ad, k * kStepDesc), desc_add(bd, k * kStepDesc), idesc,
+                                  sfa + (atom * 4 + (sfid << 30)), sfb + (atom * kNB * 4 + (sfid << 30)), acc);
   }
+}
+
+template <int VEC, int NK, int M, int N, int kNB, bool PAIR>
+__device__ __forceinline__ void issue_kblock(uint32_t d_tmem, uint64_t ad, uint64_t bd, uint32_t sfa, uint32_t sfb,
+                                             bool first) {
+  issue_mmas<VEC, 0, NK, M, N, kNB, PAIR>(d_tmem, ad, bd, sfa, sfb, first);
 }
 
 template <int VEC, int M, int N, int kNB, bool PAIR>
-__device__ __forceinline__ void issue_kblock_any(int nk, uint32_t d_tmem, uint32_t a_s, uint32_t b_s, uint32_t sfa_t,
-                                                 uint32_t sfb_t, bool first) {
+__device__ __forceinline__ void issue_kblock_any(int nk, uint32_t d_tmem, uint64_t ad, uint64_t bd, uint32_t sfa,
+                                                 uint32_t sfb, bool first) {
   switch (nk) {
-    case 4: issue_kblock<VEC, 4, M, N, kNB, PAIR>(d_tmem, a_s, b_s, sfa_t, sfb_t, first); break;
-    case 3: issue_kblock<VEC, 3, M, N, kNB, PAIR>(d_tmem, a_s, b_s, sfa_t, sfb_t, first); break;
-    case 2: issue_kblock<VEC, 2, M, N, kNB, PAIR>(d_tmem, a_s, b_s, sfa_t, sfb_t, first); break;
-    case 1: issue_kblock<VEC, 1, M, N, kNB, PAIR>(d_tmem, a_s, b_s, sfa_t, sfb_t, first); break;
+    case 4: issue_kblock<VEC, 4, M, N, kNB, PAIR>(d_tmem, ad, bd, sfa, sfb, first); break;
+    case 3: issue_kblock<VEC, 3, M, N, kNB, PAIR>(d_tmem, ad, bd, sfa, sfb, first); break;
+    case 2: issue_kblock<VEC, 2, M, N, kNB, PAIR>(d_tmem, ad, bd, sfa, sfb, first); break;
+    case 1: issue_kblock<VEC, 1, M, N, kNB, PAIR>(d_tmem, ad, bd, sfa, sfb, first); break;
     default: break;
   }
 }
@@ -237,6 +253,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0, acc_phase = 0;
+      const uint64_t adesc0 = sm100::smem_desc(sm100::smem_u32(smem + C::kOffA), 16, 1024, 2);
+      const uint64_t bdesc0 = sm100::smem_desc(sm100::smem_u32(smem + C::kOffB), 16, 1024, 2);
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
         sm100::mbar_wait(tempty, acc_phase ^ 1);
         sm100::tc_fence_after();
@@ -259,13 +277,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                                             sm100::smem_desc(sfb_s + (j * C::kAtomsPerKb + a) * 512, 0, 128, 0));
             }
           }
-          const uint32_t a_s = sm100::smem_u32(smem + C::kOffA + stage * C::kABytes);
-          const uint32_t b_s = sm100::smem_u32(smem + C::kOffB + stage * C::kBBytes);
+          const uint64_t ad = desc_add(adesc0, (uint32_t)(stage * (C::kABytes >> 4)));
+          const uint64_t bd = desc_add(bdesc0, (uint32_t)(stage * (C::kBBytes >> 4)));
           if (g.debug == 2 || g.debug == 4) {
           } else if (kb + 1 < g.num_kb || g.tail_mmas == 0) {
-            issue_kblock<VEC, BK / UMMA_K, BM, BN, C::kNB, false>(tmem_base, a_s, b_s, sfa_t, sfb_t, kb == 0);
+            issue_kblock<VEC, BK / UMMA_K, BM, BN, C::kNB, false>(tmem_base, ad, bd, sfa_t, sfb_t, kb == 0);
           } else {
-            issue_kblock_any<VEC, BM, BN, C::kNB, false>(g.tail_mmas, tmem_base, a_s, b_s, sfa_t, sfb_t, kb == 0);
+            issue_kblock_any<VEC, BM, BN, C::kNB, false>(g.tail_mmas, tmem_base, ad, bd, sfa_t, sfb_t, kb == 0);
           }
           sm100::tc_commit(&empty[stage]);
           if (++stage == C::kStages) { stage = 0; phase ^= 1; }
@@ -308,53 +326,121 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 
 // ---------------------------------------------------------------------------
-// 2-CTA (cta_group::2) kernel: a CTA pair computes a 256 x 256 output tile.
-//   warp 0      TMA producer (both CTAs): own 128 rows of A and of B (cta_group::2
-//               loads counted on the leader's `full` barrier) and this CTA's scale
-//               factors (SFA for its 128 rows, SFB for all 256 rows) on its own `sf_full`
-//   warp 1      TMEM allocator (both) + MMA issuer (leader, one thread):
-//               tcgen05.mma.cta_group::2 M=256 N=256 K=64, commit multicast to both CTAs
+// 2-CTA (cta_group::2) kernel: a CTA pair computes a 256 x 256 output tile, persistent
+// over tiles.  K advances in 512-wide stages (two 128-B K slices per row).
+//   warp 0      TMA producer (both CTAs): one 3-D box of 128 rows x 2 slices each for A
+//               and B (cta_group::2: completion bytes counted on the leader's `full`),
+//               this CTA's scale factors (SFA for its 128 rows, SFB for all 256 rows) by
+//               1-D bulk copies into an SF slot (`sf_full`)
+//   warp 1      TMEM allocator (both) + MMA issuer (leader, whole warp converged, one
+//               elected lane issues): 8 x tcgen05.mma.cta_group::2 M=256 N=256 K=64 per
+//               stage, commits multicast to both CTAs (`empty` for the A/B stage,
+//               `tsf_empty` for the TMEM SF slot)
 //   warps 2-5   scale-factor stagers (per CTA, one per TMEM lane quadrant): SMEM -> regs
-//               -> tcgen05.st into the stage's TMEM slot, then arrive on the leader's
-//               leader's `full` barrier.  (tcgen05.cp costs ~86 tensor-pipe cycles per 512-B
-//               atom -- 60-120% of the MMA time -- so the copy is moved off the pipe.)
-//   warps 6-9   epilogue (per CTA): TMEM -> regs -> * ts_A*ts_W -> bf16/f32 -> global
+//               -> tcgen05.st into a TMEM SF slot, then arrive on the leader's `full`
+//               (tcgen05.cp costs ~16 tensor-pipe cycles per 512-B atom, 24 atoms per
+//               NVFP4 stage -- it would cost ~35% of the MMA time, so it is off the pipe)
+//   warps 6-13  epilogue (per CTA): TMEM -> regs -> * ts_A*ts_W -> bf16 (released to the
+//               next tile's MMAs before the global stores) / f32 -> global
+// A/B SMEM stages and SF slots are decoupled: 3 A/B stages of 64 KB (~97 B/cycle/SM of
+// TMA throughput measured for this box shape) and 2-3 SF slots, sized so NVFP4's SF
+// (96 TMEM columns per stage) fit next to the 256-column accumulator.
 // ---------------------------------------------------------------------------
 template <int VEC>
 struct Cfg2 {
-  static constexpr int kAtomsPerKb = BK / VEC / 4;           // SF atoms (128 rows x 4 cols) per k-block
-  static constexpr int kStages = VEC == 16 ? 5 : 6;
-  static constexpr int kABytes = 128 * BK_BYTES;
-  static constexpr int kBBytes = 128 * BK_BYTES;
-  static constexpr int kSfaBytes = kAtomsPerKb * 512;
-  static constexpr int kSfbBytes = 2 * kAtomsPerKb * 512;
-  static constexpr int kSfaCols = kAtomsPerKb * 4;
-  static constexpr int kSfbCols = 2 * kAtomsPerKb * 4;
-  static constexpr int kSfCols = kSfaCols + kSfbCols;          // TMEM columns per stage slot
+  static constexpr int kBK = 512;                                // FP4 elements per stage
+  static constexpr int kSlices = kBK / BK;                       // 128-B K slices per stage
+  static constexpr int kMmas = kBK / UMMA_K;                     // MMAs per stage
+  static constexpr int kAtoms = kBK / VEC / 4;                   // SF atoms (128 rows x 4 cols) per stage
+  static constexpr int kStages = 3;                              // A/B stages
+  static constexpr int kSfSlots = VEC == 16 ? 2 : 3;             // SF slots (SMEM and TMEM)
+  static constexpr int kABytes = 128 * kBK / 2;
+  static constexpr int kBBytes = 128 * kBK / 2;
+  static constexpr int kSfaBytes = kAtoms * 512;
+  static constexpr int kSfbBytes = 2 * kAtoms * 512;
+  static constexpr int kSfaCols = kAtoms * 4;
+  static constexpr int kSfbCols = 2 * kAtoms * 4;
+  static constexpr int kSfCols = kSfaCols + kSfbCols;          // TMEM columns per SF slot
   static constexpr int kAccCols = 256;
   static constexpr int kTmemCols = 512;
-  static_assert(kAccCols + kStages * kSfCols <= kTmemCols, "TMEM budget");
+  static_assert(kAccCols + kSfSlots * kSfCols <= kTmemCols, "TMEM budget");
   static constexpr int kOffA = 0;
   static constexpr int kOffB = kOffA + kStages * kABytes;
   static constexpr int kOffSfa = kOffB + kStages * kBBytes;
-  static constexpr int kOffSfb = kOffSfa + kStages * kSfaBytes;
-  static constexpr int kOffBar = kOffSfb + kStages * kSfbBytes;
+  static constexpr int kOffSfb = kOffSfa + kSfSlots * kSfaBytes;
+  static constexpr int kOffBar = kOffSfb + kSfSlots * kSfbBytes;
   static constexpr int kSmem = kOffBar + 512 + 1024;
-  static constexpr int kThreads2 = 320;
+  static_assert(kSmem <= 232448, "SMEM budget");
+  static constexpr int kThreads2 = 448;
+  static constexpr int kEpiWarps = 8;   // 2 per TMEM lane quadrant, 128 accumulator columns each
+};
+
+// 3-D TMA load (box {128 B, 128 rows, kSlices}) whose completion bytes are counted on the
+// LEADER CTA's mbarrier (cta_group::2).
+__device__ __forceinline__ void tma_load_3d_2sm(void* smem_dst, const CUtensorMap* desc, uint32_t leader_mbar,
+                                                int32_t c1, int32_t c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(sm100::smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(desc)), "r"(leader_mbar), "r"(0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
+// Warp-converged MMAs k in [K0, K1) of a 512-wide stage (k-step k: K slice k / 4, 32-B
+// offset k % 4 inside the 128-B swizzled row).
+template <int VEC, int K0, int K1>
+__device__ __forceinline__ void issue_stage_mmas(uint32_t el, uint32_t d_tmem, uint64_t ad, uint64_t bd, uint32_t sfa,
+                                                 uint32_t sfb, bool first) {
+#pragma unroll
+  for (int k = K0; k < K1; ++k) {
+    constexpr uint32_t kSliceDesc = (128 * BK_BYTES) >> 4;   // 16 KB between K slices
+    const uint32_t off = (uint32_t)(k >> 2) * kSliceDesc + (uint32_t)(k & 3) * 2u;
+    const uint32_t atom = VEC == 16 ? k : (k >> 1);
+    const uint32_t sfid = VEC == 16 ? 0u : (uint32_t)(k & 1) * 2u;
+    const uint32_t idesc = sm100::idesc_fp4(256, 256, VEC == 32, sfid, sfid);
+    const uint32_t acc = (K0 == 0 && k == 0 && first) ? 0u : 1u;
+    sm100::tc_mma_fp4_2sm_if<VEC>(el, d_tmem, desc_add(ad, off), desc_add(bd, off), idesc,
+                                  sfa + (atom * 4 + (sfid << 30)), sfb + (atom * 8 + (sfid << 30)), acc);
+  }
+}
+
+template <int VEC>
+__device__ __forceinline__ void issue_stage_tail(int nk, uint32_t el, uint32_t d_tmem, uint64_t ad, uint64_t bd,
+                                                 uint32_t sfa, uint32_t sfb, bool first) {
+  switch (nk) {  // MMAs in the last stage (0 = full)
+    case 1: issue_stage_mmas<VEC, 0, 1>(el, d_tmem, ad, bd, sfa, sfb, first); break;
+    case 2: issue_stage_mmas<VEC, 0, 2>(el, d_tmem, ad, bd, sfa, sfb, first); break;
+    case 3: issue_stage_mmas<VEC, 0, 3>(el, d_tmem, ad, bd, sfa, sfb, first); break;
+    case 4: issue_stage_mmas<VEC, 0, 4>(el, d_tmem, ad, bd, sfa, sfb, first); break;
+    case 5: issue_stage_mmas<VEC, 0, 5>(el, d_tmem, ad, bd, sfa, sfb, first); break;
+    case 6: issue_stage_mmas<VEC, 0, 6>(el, d_tmem, ad, bd, sfa, sfb, first); break;
+    case 7: issue_stage_mmas<VEC, 0, 7>(el, d_tmem, ad, bd, sfa, sfb, first); break;
+    default: issue_stage_mmas<VEC, 0, 8>(el, d_tmem, ad, bd, sfa, sfb, first); break;
+  }
+}
+
+// Ring position: slot index and parity, advanced once per stage.
+struct Ring {
+  int idx = 0;
+  uint32_t ph = 0;
+  template <int N>
+  __device__ __forceinline__ void next() {
+    if (++idx == N) { idx = 0; ph ^= 1; }
+  }
 };
 
 template <int VEC, int OUT>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
-    k_gemm_fp4_2sm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const __grid_constant__ CUtensorMap tmSFA, const __grid_constant__ CUtensorMap tmSFB, GemmArgs g) {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(448, 1)
+    k_gemm_fp4_2sm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs g) {
   using C = Cfg2<VEC>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  // full[s] (leader's): both CTAs' A/B bytes landed AND both CTAs' scale factors staged in TMEM
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
-  uint64_t* empty = full + C::kStages;                               // stage free (MMA committed)
-  uint64_t* sf_full = empty + C::kStages;                            // this CTA's SF landed in SMEM
-  uint64_t* tfull = sf_full + C::kStages;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kOffBar);   // leader's: A/B landed + SF staged (both CTAs)
+  uint64_t* empty = full + C::kStages;                               // A/B stage free (MMAs committed)
+  uint64_t* sf_full = empty + C::kStages;                            // this CTA's SF landed in SMEM slot
+  uint64_t* sf_empty = sf_full + C::kSfSlots;                        // SF SMEM slot read by the stagers
+  uint64_t* tsf_empty = sf_empty + C::kSfSlots;                      // TMEM SF slot free (MMAs committed)
+  uint64_t* tfull = tsf_empty + C::kSfSlots;
   uint64_t* tempty = tfull + 1;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 1);
 
@@ -370,15 +456,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
   if (warp == 0 && lane == 0) {
     sm100::tma_prefetch_desc(&tmA);
     sm100::tma_prefetch_desc(&tmB);
-    sm100::tma_prefetch_desc(&tmSFA);
-    sm100::tma_prefetch_desc(&tmSFB);
     for (int s = 0; s < C::kStages; ++s) {
       sm100::mbar_init(&full[s], 9);      // leader producer (A/B bytes) + 4 stager warps x 2 CTAs
       sm100::mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < C::kSfSlots; ++s) {
       sm100::mbar_init(&sf_full[s], 1);
+      sm100::mbar_init(&sf_empty[s], 4);  // this CTA's 4 stager warps
+      sm100::mbar_init(&tsf_empty[s], 1);
     }
     sm100::mbar_init(tfull, 1);
-    sm100::mbar_init(tempty, 8);          // 4 epilogue warps x 2 CTAs
+    sm100::mbar_init(tempty, 2 * C::kEpiWarps);  // epilogue warps x 2 CTAs
     sm100::fence_mbar_init();
   }
   if (warp == 1) sm100::tmem_alloc_2sm(tmem_holder, C::kTmemCols);
@@ -393,88 +481,74 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
     if (lane == 0) {
       // ------------------------------------------------------------- producer
       pdl_wait();  // A, its scale factors and tensor scale come from the act-quant kernel
-      int stage = 0;
-      uint32_t phase = 0;
+      Ring ab, sf;
       for (int tile = cluster; tile < num_tiles; tile += nclusters) {
         const int m_blk = tile % num_m_blk, n_blk = tile / num_m_blk;
         for (int kb = 0; kb < num_kb; ++kb) {
-          unsigned long long* dbg = (g.dbg && blockIdx.x == 0 && tile == cluster && kb < 32) ? g.dbg + 256 + 2 * kb : nullptr;
-          if (dbg) dbg[0] = clock64();
-          sm100::mbar_wait(&empty[stage], phase ^ 1);
-          if (dbg) dbg[1] = clock64();
+          sm100::mbar_wait(&sf_empty[sf.idx], sf.ph ^ 1);
           {
             // Scale factors: contiguous 512-B atoms per 128-row block -> 1-D bulk copies
             // (K tail: copy only the atoms that exist; the rest of the slot is never read
             // by an issued MMA).  Row blocks past the end of A / B are skipped.
-            const int64_t katom = (int64_t)kb * C::kAtomsPerKb;
-            const uint32_t nat = (uint32_t)imin64(C::kAtomsPerKb, sf_col_blocks - katom) * 512u;
+            const int64_t katom = (int64_t)kb * C::kAtoms;
+            const uint32_t nat = (uint32_t)imin64(C::kAtoms, sf_col_blocks - katom) * 512u;
             const int64_t ra = (int64_t)m_blk * 2 + rank;
             const int64_t rb0 = (int64_t)n_blk * 2;
             const uint32_t bytes = (ra < a_row_blocks ? nat : 0u) + (rb0 < b_row_blocks ? nat : 0u) +
                                    (rb0 + 1 < b_row_blocks ? nat : 0u);
-            sm100::mbar_arrive_expect_tx(&sf_full[stage], bytes);
+            sm100::mbar_arrive_expect_tx(&sf_full[sf.idx], bytes);
             if (ra < a_row_blocks)
-              sm100::bulk_load(smem + C::kOffSfa + stage * C::kSfaBytes, g.a_sf + (ra * sf_col_blocks + katom) * 512,
-                               nat, &sf_full[stage]);
+              sm100::bulk_load(smem + C::kOffSfa + sf.idx * C::kSfaBytes, g.a_sf + (ra * sf_col_blocks + katom) * 512,
+                               nat, &sf_full[sf.idx]);
 #pragma unroll
             for (int j = 0; j < 2; ++j)
               if (rb0 + j < b_row_blocks)
-                sm100::bulk_load(smem + C::kOffSfb + stage * C::kSfbBytes + j * C::kSfaBytes,
-                                 g.b_sf + ((rb0 + j) * sf_col_blocks + katom) * 512, nat, &sf_full[stage]);
+                sm100::bulk_load(smem + C::kOffSfb + sf.idx * C::kSfbBytes + j * C::kSfaBytes,
+                                 g.b_sf + ((rb0 + j) * sf_col_blocks + katom) * 512, nat, &sf_full[sf.idx]);
           }
-          if (leader) sm100::mbar_arrive_expect_tx(&full[stage], 2u * (C::kABytes + C::kBBytes));
-          const uint32_t lb = sm100::leader_bar(&full[stage]);
-          sm100::tma_load_2d_2sm(smem + C::kOffA + stage * C::kABytes, &tmA, lb, kb * BK_BYTES,
-                                 m_blk * 256 + (int)rank * 128);
-          sm100::tma_load_2d_2sm(smem + C::kOffB + stage * C::kBBytes, &tmB, lb, kb * BK_BYTES,
-                                 n_blk * 256 + (int)rank * 128);
-          if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+          sf.next<C::kSfSlots>();
+          sm100::mbar_wait(&empty[ab.idx], ab.ph ^ 1);
+          if (leader) sm100::mbar_arrive_expect_tx(&full[ab.idx], 2u * (C::kABytes + C::kBBytes));
+          const uint32_t lb = sm100::leader_bar(&full[ab.idx]);
+          tma_load_3d_2sm(smem + C::kOffA + ab.idx * C::kABytes, &tmA, lb, m_blk * 256 + (int)rank * 128,
+                          kb * C::kSlices);
+          tma_load_3d_2sm(smem + C::kOffB + ab.idx * C::kBBytes, &tmB, lb, n_blk * 256 + (int)rank * 128,
+                          kb * C::kSlices);
+          ab.next<C::kStages>();
         }
       }
     }
   } else if (warp == 1) {
-    if (leader && lane == 0) {
+    if (leader) {
       // ---------------------------------------------------------- MMA issuer
-      int stage = 0;
-      uint32_t phase = 0, acc_phase = 0;
-      int ntl = 0;
-      for (int tile = cluster; tile < num_tiles; tile += nclusters, ++ntl) {
-        if (g.dbg && blockIdx.x == 0 && ntl < 4) {
-          uint64_t gt; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-          g.dbg[400 + 4 * ntl] = clock64(); g.dbg[401 + 4 * ntl] = gt;
-        }
+      // The whole warp runs the loop (converged, uniform descriptors); one elected lane
+      // issues.  A stage's 8 MMAs (~1000 cycles of tensor work) are queued before the
+      // thread waits for the next stage, so barrier latency never starves the pipe.
+      const uint32_t el = sm100::elect_lane();
+      Ring ab, sf;
+      uint32_t acc_phase = 0;
+      const uint64_t adesc0 = sm100::smem_desc(sm100::smem_u32(smem + C::kOffA), 16, 1024, 2);
+      const uint64_t bdesc0 = sm100::smem_desc(sm100::smem_u32(smem + C::kOffB), 16, 1024, 2);
+      const uint32_t sf0 = tmem_base + C::kAccCols;
+      for (int tile = cluster; tile < num_tiles; tile += nclusters) {
         sm100::mbar_wait(tempty, acc_phase ^ 1);
-        if (g.dbg && blockIdx.x == 0 && ntl < 4) g.dbg[402 + 4 * ntl] = clock64();
-        sm100::tc_fence_after();
-        sm100::mbar_wait(&full[stage], phase);
         for (int kb = 0; kb < num_kb; ++kb) {
+          sm100::mbar_wait(&full[ab.idx], ab.ph);
           sm100::tc_fence_after();
-          const uint32_t sfa_t = tmem_base + C::kAccCols + stage * C::kSfCols;
-          const uint32_t sfb_t = sfa_t + C::kSfaCols;
-          const uint32_t a_s = sm100::smem_u32(smem + C::kOffA + stage * C::kABytes);
-          const uint32_t b_s = sm100::smem_u32(smem + C::kOffB + stage * C::kBBytes);
-          const int cur = stage;
-          if (++stage == C::kStages) { stage = 0; phase ^= 1; }
-          if (kb + 1 < num_kb) {
-            // Issue 3 MMAs, then wait for the next stage while they execute (keeps the
-            // shallow tcgen05 issue queue non-empty across the barrier wait).
-            issue_kblock<VEC, 3, 256, 256, 2, true>(tmem_base, a_s, b_s, sfa_t, sfb_t, kb == 0);
-            sm100::mbar_wait(&full[stage], phase);
-            issue_kblock_from<VEC, 3, 4, 256, 256, 2, true>(tmem_base, a_s, b_s, sfa_t, sfb_t, false);
-          } else if (tail_mmas == 0) {
-            issue_kblock<VEC, BK / UMMA_K, 256, 256, 2, true>(tmem_base, a_s, b_s, sfa_t, sfb_t, kb == 0);
-          } else {
-            issue_kblock_any<VEC, 256, 256, 2, true>(tail_mmas, tmem_base, a_s, b_s, sfa_t, sfb_t, kb == 0);
-          }
-          sm100::tc_commit_2sm_mc(&empty[cur], 0x3);
+          const uint32_t sfa_t = sf0 + sf.idx * C::kSfCols, sfb_t = sfa_t + C::kSfaCols;
+          const uint64_t ad = desc_add(adesc0, (uint32_t)(ab.idx * (C::kABytes >> 4)));
+          const uint64_t bd = desc_add(bdesc0, (uint32_t)(ab.idx * (C::kBBytes >> 4)));
+          if (kb + 1 < num_kb || tail_mmas == 0)
+            issue_stage_mmas<VEC, 0, C::kMmas>(el, tmem_base, ad, bd, sfa_t, sfb_t, kb == 0);
+          else
+            issue_stage_tail<VEC>(tail_mmas, el, tmem_base, ad, bd, sfa_t, sfb_t, kb == 0);
+          sm100::tc_commit_2sm_mc_if(el, &empty[ab.idx], 0x3);
+          sm100::tc_commit_2sm_mc_if(el, &tsf_empty[sf.idx], 0x3);
+          ab.next<C::kStages>();
+          sf.next<C::kSfSlots>();
         }
-        sm100::tc_commit_2sm_mc(tfull, 0x3);
-        if (g.dbg && blockIdx.x == 0 && ntl < 4) g.dbg[403 + 4 * ntl] = clock64();
+        sm100::tc_commit_2sm_mc_if(el, tfull, 0x3);
         acc_phase ^= 1;
-      }
-      if (g.dbg && blockIdx.x == 0) {
-        uint64_t gt; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-        g.dbg[420] = clock64(); g.dbg[421] = gt; g.dbg[422] = ntl;
       }
     }
   } else if (warp < 6) {
@@ -483,51 +557,51 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
     // would produce): lane 32q+l, column c+j of a 128-row atom holds the 4 scale
     // codes of row l+32j -- i.e. bytes [16l, 16l+16) of the 512-B SMEM atom.
     const int q = warp & 3;
-    int stage = 0;
-    uint32_t phase = 0;
+    Ring ab, sf;
+    const uint32_t sa0 = sm100::smem_u32(smem + C::kOffSfa) + lane * 16, sb0 = sm100::smem_u32(smem + C::kOffSfb) + lane * 16;
     for (int tile = cluster; tile < num_tiles; tile += nclusters) {
       for (int kb = 0; kb < num_kb; ++kb) {
-        unsigned long long* dbg = (g.dbg && blockIdx.x == 0 && q == 0 && lane == 0 && tile == cluster && kb < 32) ? g.dbg + 128 + 4 * kb : nullptr;
-        if (dbg) dbg[0] = clock64();
-        sm100::mbar_wait(&sf_full[stage], phase);
-        if (dbg) dbg[1] = clock64();
-        const uint8_t* sa = smem + C::kOffSfa + stage * C::kSfaBytes + lane * 16;
-        const uint8_t* sb = smem + C::kOffSfb + stage * C::kSfbBytes + lane * 16;
+        sm100::mbar_wait(&sf_full[sf.idx], sf.ph);
+        const uint32_t sa = sa0 + sf.idx * C::kSfaBytes, sb = sb0 + sf.idx * C::kSfbBytes;
         uint32_t ra[C::kSfaCols], rb[C::kSfbCols];
 #pragma unroll
-        for (int a = 0; a < C::kAtomsPerKb; ++a) {
-          const uint4 va = *reinterpret_cast<const uint4*>(sa + a * 512);
+        for (int a = 0; a < C::kAtoms; ++a) {
+          const uint4 va = sm100::lds128(sa + a * 512);
           ra[4 * a + 0] = va.x; ra[4 * a + 1] = va.y; ra[4 * a + 2] = va.z; ra[4 * a + 3] = va.w;
 #pragma unroll
           for (int j = 0; j < 2; ++j) {  // TMEM order: atom-major, then 128-row block
-            const uint4 vb = *reinterpret_cast<const uint4*>(sb + (j * C::kAtomsPerKb + a) * 512);
+            const uint4 vb = sm100::lds128(sb + (j * C::kAtoms + a) * 512);
             rb[8 * a + 4 * j + 0] = vb.x; rb[8 * a + 4 * j + 1] = vb.y;
             rb[8 * a + 4 * j + 2] = vb.z; rb[8 * a + 4 * j + 3] = vb.w;
           }
         }
-        const uint32_t t0 = tmem_base + ((uint32_t)(q * 32) << 16) + C::kAccCols + stage * C::kSfCols;
-        sm100::tmem_st_32x32b<C::kSfaCols>(t0, ra);
-        if constexpr (C::kSfbCols == 32) {
-          sm100::tmem_st_32x32b<16>(t0 + C::kSfaCols, rb);
-          sm100::tmem_st_32x32b<16>(t0 + C::kSfaCols + 16, rb + 16);
-        } else {
-          sm100::tmem_st_32x32b<C::kSfbCols>(t0 + C::kSfaCols, rb);
-        }
-        if (dbg) dbg[2] = clock64();
+        __syncwarp();
+        if (lane == 0) sm100::mbar_arrive(&sf_empty[sf.idx]);   // SMEM slot consumed (values in registers)
+        sm100::mbar_wait(&tsf_empty[sf.idx], sf.ph ^ 1);        // TMEM slot's previous MMAs done
+        sm100::tc_fence_after();
+        const uint32_t t0 = tmem_base + ((uint32_t)(q * 32) << 16) + C::kAccCols + sf.idx * C::kSfCols;
+#pragma unroll
+        for (int c = 0; c < C::kSfaCols; c += 16) sm100::tmem_st_32x32b<16>(t0 + c, ra + c);
+#pragma unroll
+        for (int c = 0; c < C::kSfbCols; c += 16) sm100::tmem_st_32x32b<16>(t0 + C::kSfaCols + c, rb + c);
         sm100::tmem_st_wait();
-        if (dbg) dbg[3] = clock64();
         sm100::tc_fence_before();
         __syncwarp();
         if (lane == 0) {
-          if (leader) sm100::mbar_arrive(&full[stage]);
-          else sm100::mbar_arrive_remote(&full[stage], 0);
+          if (leader) sm100::mbar_arrive(&full[ab.idx]);
+          else sm100::mbar_arrive_remote(&full[ab.idx], 0);
         }
-        if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+        ab.next<C::kStages>();
+        sf.next<C::kSfSlots>();
       }
     }
   } else {
     // ------------------------------------------------------ epilogue (both CTAs)
-    const int q = warp & 3;
+    // Warp w reads TMEM lane quadrant w % 4 (hardware rule), columns [h*128, h*128+128).
+    // bf16 output: the 128 columns are pulled into registers (as bf16 pairs) and the
+    // accumulator is released BEFORE the global stores, so the next tile's MMAs start
+    // while this tile's output is being written.
+    const int q = warp & 3, h = (warp - 6) >> 2;
     pdl_wait();
     const float alpha = __ldg(g.a_ts) * __ldg(g.b_ts);
     uint32_t acc_phase = 0;
@@ -536,19 +610,49 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
       sm100::mbar_wait(tfull, acc_phase);
       sm100::tc_fence_after();
       const int64_t row = (int64_t)m_blk * 256 + rank * 128 + q * 32 + lane;
+      const int64_t col0 = (int64_t)n_blk * 256 + h * 128;
+      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + h * 128;
+      if constexpr (OUT == MRFP4_DT_BF16) {
+        uint32_t pkd[64];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t r[32];
+          sm100::tmem_ld_32x32b_x32(taddr + c * 32, r);
+          sm100::tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            __nv_bfloat162 v = __floats2bfloat162_rn(__uint_as_float(r[2 * j]) * alpha,
+                                                     __uint_as_float(r[2 * j + 1]) * alpha);
+            pkd[16 * c + j] = *reinterpret_cast<uint32_t*>(&v);
+          }
+        }
+        sm100::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (leader) sm100::mbar_arrive(tempty);
+          else sm100::mbar_arrive_remote(tempty, 0);
+        }
+        if (row < g.M) {
+          __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(g.d) + row * g.ldd + col0;
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (col0 + 8 * j < g.N)
+              *reinterpret_cast<uint4*>(dst + 8 * j) = make_uint4(pkd[4 * j], pkd[4 * j + 1], pkd[4 * j + 2], pkd[4 * j + 3]);
+        }
+      } else {
 #pragma unroll 1
-      for (int c = 0; c < 256; c += 32) {
-        uint32_t r[32];
-        sm100::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + c, r);
-        sm100::tmem_ld_wait();
-        const int64_t col = (int64_t)n_blk * 256 + c;
-        if (row < g.M) store_row32<OUT>(g, row, col, r, alpha);
-      }
-      sm100::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if (leader) sm100::mbar_arrive(tempty);
-        else sm100::mbar_arrive_remote(tempty, 0);
+        for (int c = 0; c < 128; c += 32) {
+          uint32_t r[32];
+          sm100::tmem_ld_32x32b_x32(taddr + c, r);
+          sm100::tmem_ld_wait();
+          if (row < g.M) store_row32<OUT>(g, row, col0 + c, r, alpha);
+        }
+        sm100::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (leader) sm100::mbar_arrive(tempty);
+          else sm100::mbar_arrive_remote(tempty, 0);
+        }
       }
       acc_phase ^= 1;
     }
@@ -593,17 +697,17 @@ bool make_code_map(CUtensorMap* tm, const uint8_t* ptr, int64_t rows, int64_t K,
   return r == CUDA_SUCCESS;
 }
 
-// Swizzled scale factors viewed as [128-row blocks][col_blocks * 64] uint64 (one 512-B atom = 64 x u64).
-bool make_sf_map(CUtensorMap* tm, const uint8_t* sf, int64_t rows, int64_t sf_cols, int atoms, int box_rows) {
+// Codes [rows, K/2] viewed as [K/256 slices][rows][128 B] (3-D, K % 256 == 0): one box =
+// `slices` consecutive 128-B K slices of `box_rows` rows, 128-B swizzled.
+bool make_code_map3(CUtensorMap* tm, const uint8_t* ptr, int64_t rows, int64_t K, int box_rows, int slices) {
   auto encode = get_encode_fn();
   if (!encode) return false;
-  const int64_t rb = ceil_div(rows, 128), cb = ceil_div(sf_cols, 4);
-  cuuint64_t dims[2] = {(cuuint64_t)(cb * 64), (cuuint64_t)rb};
-  cuuint64_t strides[1] = {(cuuint64_t)(cb * 512)};
-  cuuint32_t box[2] = {(cuuint32_t)(atoms * 64), (cuuint32_t)box_rows};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = encode(tm, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<uint8_t*>(sf), dims, strides, box, estr,
-                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+  cuuint64_t dims[3] = {(cuuint64_t)BK_BYTES, (cuuint64_t)rows, (cuuint64_t)(K / BK)};
+  cuuint64_t strides[2] = {(cuuint64_t)(K / 2), (cuuint64_t)BK_BYTES};
+  cuuint32_t box[3] = {(cuuint32_t)BK_BYTES, (cuuint32_t)box_rows, (cuuint32_t)slices};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = encode(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(ptr), dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -657,24 +761,22 @@ int launch2(const uint8_t* a, const uint8_t* b, const GemmArgs& args0, cudaStrea
     attr_set = true;
   }
   GemmArgs g = args0;
-  CUtensorMap tmA, tmB, tmSFA, tmSFB;
+  CUtensorMap tmA, tmB;
   const int64_t sfc = g.K / VEC;
-  if (!make_code_map(&tmA, a, g.M, g.K, 128) || !make_code_map(&tmB, b, g.N, g.K, 128) ||
-      !make_sf_map(&tmSFA, g.a_sf, g.M, sfc, C::kAtomsPerKb, 1) ||
-      !make_sf_map(&tmSFB, g.b_sf, g.N, sfc, C::kAtomsPerKb, 2))
+  if (!make_code_map3(&tmA, a, g.M, g.K, 128, C::kSlices) || !make_code_map3(&tmB, b, g.N, g.K, 128, C::kSlices))
     return MRFP4_ECUDA;
   g.num_m_blk = (int)ceil_div(g.M, 256);
   g.num_n_blk = (int)ceil_div(g.N, 256);
-  g.num_kb = (int)ceil_div(g.K, BK);
-  g.tail_mmas = (int)((g.K % BK) / UMMA_K);
+  g.num_kb = (int)ceil_div(g.K, C::kBK);
+  g.tail_mmas = (int)((g.K % C::kBK) / UMMA_K);
   g.sf_col_blocks = ceil_div(sfc, 4);
   g.b_row_blocks = ceil_div(g.N, 128);
   const int tiles = g.num_m_blk * g.num_n_blk;
   const int clusters = std::min(tiles, num_sms() / 2);
   int nclu = clusters;
   if (g_force_grid > 0) nclu = std::min(nclu, std::max(1, g_force_grid / 2));
-  return launch_pdl(k_gemm_fp4_2sm<VEC, OUT>, dim3(2 * nclu), dim3(C::kThreads2), C::kSmem, s, tmA, tmB, tmSFA,
-                    tmSFB, g) == cudaSuccess
+  return launch_pdl(k_gemm_fp4_2sm<VEC, OUT>, dim3(2 * nclu), dim3(C::kThreads2), C::kSmem, s, tmA, tmB, g) ==
+                 cudaSuccess
              ? MRFP4_OK
              : MRFP4_ECUDA;
 }
@@ -701,7 +803,8 @@ int launch_gemm_fp4(const uint8_t* a, const uint8_t* a_sf, const float* a_ts, co
   g.N = N;
   g.K = K;
   g.ldd = ldd;
-  const bool pair = g_force_kernel ? g_force_kernel == 2 : M > 128;
+  // The 2-CTA kernel streams 512-wide K stages as 3-D boxes of 128-B slices: K % 256 == 0.
+  const bool pair = (K % 256 == 0) && (g_force_kernel ? g_force_kernel == 2 : M > 128);
   if (pair) {
     if (fmt == MRFP4_FMT_NVFP4)
       return d_dtype == MRFP4_DT_BF16 ? launch2<16, MRFP4_DT_BF16>(a, b, g, s) : launch2<16, MRFP4_DT_F32>(a, b, g, s);

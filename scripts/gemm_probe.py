@@ -33,9 +33,9 @@ for M, K, N, fmt in [(2048, 14336, 4096, "mxfp4"), (4096, 8192, 8192, "nvfp4"), 
     act_quant_into(x, w.fmt, 0, a.codes, a.sf, a.tensor_scale_dev, a.scratch)
     out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
     res = {}
-    for mode in (0, 1, 2, 3, 4, 5, 6):
+    for mode in (0, 1, 64):
         L.mrfp4_debug_gemm_mode(mode)
         t = timeit(lambda: P.gemm(a, w, out))
         res[mode] = (t * 1e6, 2 * M * N * K / t / 1e12)
     L.mrfp4_debug_gemm_mode(0)
-    print(json.dumps(dict(M=M, K=K, N=N, fmt=fmt, normal=res[0], no_loads=res[1], no_mma=res[2], mma_only=res[3], pipeline_only=res[4], mma_no_cp=res[5], full_no_cp=res[6])), flush=True)
+    print(json.dumps(dict(M=M, K=K, N=N, fmt=fmt, normal=res[0], no_ld=res[1], no_mma=res[64])), flush=True)
