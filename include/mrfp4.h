@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define MRFP4_ABI_VERSION 1
+#define MRFP4_ABI_VERSION 2
 
 /* return codes */
 #define MRFP4_OK 0
@@ -73,9 +73,10 @@ int mrfp4_group_size(int fmt);
 /* Bytes of a swizzled scale-factor buffer for a [rows, sf_cols] scale matrix. */
 size_t mrfp4_sf_bytes(int64_t rows, int64_t sf_cols);
 
-/* Device workspace needed by mrfp4_act_quant (NVFP4: 8 bytes, the tensor max and an
- * arrival counter).  It must be zero-filled once before first use; every successful
- * call leaves it zeroed again, so one workspace serves a stream's calls in order. */
+/* Device workspace needed by mrfp4_act_quant (NVFP4: 16 bytes -- the tensor max and the
+ * counters of the in-kernel grid barrier).  It must be zero-filled once before first use;
+ * every successful call leaves it re-armed, so one workspace serves a stream's calls in
+ * order (not concurrent calls). */
 size_t mrfp4_act_quant_workspace(int64_t M, int64_t K, int fmt);
 
 /*
@@ -84,7 +85,8 @@ size_t mrfp4_act_quant_workspace(int64_t M, int64_t K, int fmt);
  * E2M1 codes, 2 per byte.  had_k in {0 (no rotation), 16, 32, 64, 128}.
  * x: [M, K] with row stride ldx elements (ldx*elt_size % 16 == 0), dtype x_dtype.
  * tensor_scale: device float, receives f32(4/3) (MXFP4) or the NVFP4 global scale.
- * NVFP4 runs two stream-ordered passes (whole-tensor max, then encode).
+ * NVFP4 runs both passes (whole-tensor max, then encode) in one persistent launch with a
+ * grid barrier.
  * Kernels are launched with programmatic dependent launch (PDL); set MRFP4_PDL=0 in
  * the environment to launch them with plain stream ordering.
  */
@@ -105,11 +107,14 @@ int mrfp4_sf_unswizzle(const uint8_t* sf_swizzled, uint8_t* sf_rowmajor,
  * a: [M, K/2] codes + swizzled sf; b: [N, K/2] codes + swizzled sf (the weight);
  * a_ts, b_ts: device float tensor scales; d: [M, N] row stride ldd, dtype d_dtype
  * (MRFP4_DT_BF16 or MRFP4_DT_F32).  Requires K % 64 == 0, N % 8 == 0.
+ * workspace: device scratch of mrfp4_gemm_workspace() bytes for small-M split-K (fp32
+ * partial sums, reduced in a fixed order); NULL or too small = no split (slower at small M).
  */
+size_t mrfp4_gemm_workspace(int64_t M, int64_t N, int64_t K, int fmt);
 int mrfp4_gemm(const uint8_t* a, const uint8_t* a_sf, const float* a_ts,
                const uint8_t* b, const uint8_t* b_sf, const float* b_ts,
                void* d, int d_dtype, int64_t M, int64_t N, int64_t K, int64_t ldd,
-               int fmt, void* stream);
+               int fmt, void* workspace, size_t workspace_bytes, void* stream);
 
 /* Device dequantize (formats.py:424-442): out[r,c] = ts * scale * fp4, fp32 output. */
 int mrfp4_dequantize(const uint8_t* codes, const uint8_t* sf, const float* tensor_scale,

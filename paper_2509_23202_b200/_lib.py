@@ -34,7 +34,8 @@ SIGNATURES = {
     "mrfp4_act_quant": (_int, [_vp, _int, _i64, _i64, _i64, _int, _int, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "mrfp4_sf_swizzle": (_int, [_vp, _vp, _i64, _i64, _vp]),
     "mrfp4_sf_unswizzle": (_int, [_vp, _vp, _i64, _i64, _vp]),
-    "mrfp4_gemm": (_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _int, _i64, _i64, _i64, _i64, _int, _vp]),
+    "mrfp4_gemm_workspace": (_sz, [_i64, _i64, _i64, _int]),
+    "mrfp4_gemm": (_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _int, _i64, _i64, _i64, _i64, _int, _vp, _sz, _vp]),
     "mrfp4_dequantize": (_int, [_vp, _vp, _vp, _i64, _i64, _int, _vp, _vp]),
 }
 
@@ -53,7 +54,7 @@ def lib():
                 for name, (res, args) in SIGNATURES.items():
                     fn = getattr(handle, name)
                     fn.restype, fn.argtypes = res, args
-                if handle.mrfp4_abi_version() != 1:
+                if handle.mrfp4_abi_version() != 2:
                     raise ImportError("libmrfp4.so ABI version mismatch")
                 _lib = handle
     return _lib

@@ -503,36 +503,6 @@ __device__ __forceinline__ void for_each_seg(const AQParams& p, R&& ready, F&& b
   cp_wait<0>();
 }
 
-// NVFP4 phase 1: max |S| over the whole tensor (quantizers.py:198-200 needs it first).
-template <int IN, int HK>
-__global__ void __launch_bounds__(kThreads, 4) k_tensor_absmax(AQParams p) {
-  const int lane = threadIdx.x & 31;
-  pdl_trigger();
-  float m = 0.f;
-  for_each_seg<IN, 1, false>(p, [] {}, [&](const Cursor&, uint32_t sbase) {
-    u64 P[kPairs];
-    load_pairs<IN>(sbase, lane, P);
-    if constexpr (HK > 0) fwht<HK>(P, lane, p.pm);
-    float a, b;
-    half_amax(P, a, b);   // padding rows / columns were zero-filled
-    m = max3n(a, b, m);
-  });
-  uint32_t mb = __float_as_uint(m);
-  mb = mb > 0x7f800000u ? 0x7fc00000u : mb;  // canonical NaN
-  mb = __reduce_max_sync(0xffffffffu, mb);
-  __shared__ uint32_t smax[kWarps];
-  if (lane == 0) smax[threadIdx.x >> 5] = mb;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    uint32_t x = threadIdx.x < kWarps ? smax[threadIdx.x] : 0u;
-    x = __reduce_max_sync(0xffffffffu, x);
-    if (threadIdx.x == 0 && x) {
-      atomicMax(p.gmax, x);
-      if (x >= 0x7f800000u) atomic_or_status(p.status, MRFP4_STATUS_NONFINITE);
-    }
-  }
-}
-
 // sf_offset in 32-bit arithmetic (scale buffers are < 4 GiB).
 __device__ __forceinline__ uint32_t sf_off32(uint32_t r, uint32_t c, uint32_t cb) {
   return ((r >> 7) * cb + (c >> 2)) * 512u + (r & 31u) * 16u + ((r >> 5) & 3u) * 4u + (c & 3u);
@@ -557,90 +527,186 @@ __device__ __forceinline__ void zero_sf_padding(const AQParams& p) {
   }
 }
 
-template <int IN, int FMT, int HK>
-__global__ void __launch_bounds__(kThreads, 3) k_act_quant(AQParams p) {
-  const int lane = threadIdx.x & 31;
-
-  pdl_trigger();
-  // Per-launch constants (uniform); NVFP4's depend on phase 1 (read after the PDL wait).
-  float st32 = 1.33333337306976318359375f;   // MXFP4 tensor scale f32(4/3), quantizers.py:34,191
+// Per-launch encode constants.  MXFP4: ts = f32(4/3) (quantizers.py:34,191).  NVFP4: derived
+// from the whole-tensor max exactly as numpy does (quantizers.py:187, :198-200).
+struct EncConsts {
+  float st32 = 1.33333337306976318359375f;
   double st64 = 1.0;
   float kenc = 0.f, knv = 0.f;
   uint32_t zero_code = 0;
-  auto ready = [&] {
-    if constexpr (FMT == MRFP4_FMT_NVFP4) {
-      const float smax = __uint_as_float(*(volatile uint32_t*)p.gmax);  // max |S| over the tensor
-      const double top = (double)smax * p.c64 / 6.0;      // absmax.max() / FP4_MAX
-      st32 = top > 0.0 ? __double2float_rn(top / 448.0) : 1.0f;  // f32(top / E4M3 max)
-      st64 = (double)st32;
-      zero_code = e4m3_rne64(1.0 / st64);                  // raw = 1.0 sentinel (quantizers.py:187)
-      kenc = __double2float_rn(p.c64 / 6.0 / st64);
-      knv = __double2float_rn(p.c64 / st64);
-    }
-    if (blockIdx.x == 0 && threadIdx.x == 0) *p.tensor_scale = st32;
-  };
+};
 
+__device__ __forceinline__ EncConsts nv_consts(const AQParams& p, uint32_t gmax_bits) {
+  EncConsts k;
+  const double top = (double)__uint_as_float(gmax_bits) * p.c64 / 6.0;  // absmax.max() / FP4_MAX
+  k.st32 = top > 0.0 ? __double2float_rn(top / 448.0) : 1.0f;           // f32(top / E4M3 max)
+  k.st64 = (double)k.st32;
+  k.zero_code = e4m3_rne64(1.0 / k.st64);                               // raw = 1.0 sentinel
+  k.kenc = __double2float_rn(p.c64 / 6.0 / k.st64);
+  k.knv = __double2float_rn(p.c64 / k.st64);
+  return k;
+}
+
+// Rotate (already done by the caller) -> scales -> codes -> stores of one lane segment.
+template <int FMT>
+__device__ __forceinline__ void encode_seg(const AQParams& p, const Cursor& c, const u64 (&P)[kPairs],
+                                           const EncConsts& k, uint32_t& bad) {
+  const int col0 = c.seg * kSeg;
+  if (col0 >= p.Ki || c.row >= p.Mi) return;           // idle lane (after the shuffles)
+  const bool full = col0 + kSeg <= p.Ki;                // else a 16-element tail (K % 32 == 16)
+  float a0, a1;
+  half_amax(P, a0, a1);
+  GroupScale s0, s1;
+  uint32_t sfc;
+  if constexpr (FMT == MRFP4_FMT_NVFP4) {
+    s0 = nv_group_scale(a0, p, k.kenc, k.knv, k.st32, k.st64, k.zero_code);
+    s1 = nv_group_scale(a1, p, k.kenc, k.knv, k.st32, k.st64, k.zero_code);
+    if (__float_as_uint(a0) >= 0x7f800000u || (full && __float_as_uint(a1) >= 0x7f800000u))
+      bad |= MRFP4_STATUS_NONFINITE;
+    if (s0.code == 0 || (full && s1.code == 0)) bad |= MRFP4_STATUS_SCALE_UNDERFLOW;
+    sfc = s0.code | (full ? s1.code << 8 : 0u);
+  } else {
+    const float a = max3n(a0, a1, 0.f);
+    if (__float_as_uint(a) >= 0x7f800000u) bad |= MRFP4_STATUS_NONFINITE;
+    s0 = mx_group_scale(a, p);
+    s1 = s0;
+    sfc = s0.code;
+  }
+  uint32_t w[4];
+  quantize_seg(P, s0, s1, k.st32, p, w);
+
+  uint8_t* cdst = p.codes + (uint64_t)c.row * p.half_k + (uint32_t)(col0 >> 1);
+  if (full) {
+    if ((p.Ki & 31) == 0) {
+      *reinterpret_cast<uint4*>(cdst) = make_uint4(w[0], w[1], w[2], w[3]);
+    } else {
+      reinterpret_cast<uint2*>(cdst)[0] = make_uint2(w[0], w[1]);
+      reinterpret_cast<uint2*>(cdst)[1] = make_uint2(w[2], w[3]);
+    }
+  } else {
+    *reinterpret_cast<uint2*>(cdst) = make_uint2(w[0], w[1]);
+  }
+  if constexpr (FMT == MRFP4_FMT_MXFP4) {
+    p.sf[sf_off32(c.row, c.seg, p.cb)] = (uint8_t)sfc;
+  } else {
+    // columns 2*seg, 2*seg+1 share a 16-bit word of the swizzled layout
+    *reinterpret_cast<uint16_t*>(p.sf + sf_off32(c.row, 2 * c.seg, p.cb)) = (uint16_t)sfc;
+  }
+}
+
+// MXFP4: single pass (group-local scales).
+template <int IN, int HK>
+__global__ void __launch_bounds__(kThreads, 3) k_act_quant_mx(AQParams p) {
+  const int lane = threadIdx.x & 31;
+  pdl_trigger();
+  const EncConsts k;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    pdl_wait();
+    *p.tensor_scale = k.st32;
+  }
   uint32_t bad = 0;
-  for_each_seg<IN, FMT == MRFP4_FMT_NVFP4 ? -1 : 1, FMT == MRFP4_FMT_NVFP4>(p, ready, [&](const Cursor& c, uint32_t sbase) {
+  for_each_seg<IN, 1, false>(p, [] {}, [&](const Cursor& c, uint32_t sbase) {
     u64 P[kPairs];
     load_pairs<IN>(sbase, lane, P);
     if constexpr (HK > 0) fwht<HK>(P, lane, p.pm);
-    const int col0 = c.seg * kSeg;
-    if (col0 >= p.Ki || c.row >= p.Mi) return;           // idle lane (after the shuffles)
-    const bool full = col0 + kSeg <= p.Ki;                // else a 16-element tail (K % 32 == 16)
-
-    float a0, a1;
-    half_amax(P, a0, a1);
-    GroupScale s0, s1;
-    uint32_t sfc;
-    if constexpr (FMT == MRFP4_FMT_NVFP4) {
-      s0 = nv_group_scale(a0, p, kenc, knv, st32, st64, zero_code);
-      s1 = nv_group_scale(a1, p, kenc, knv, st32, st64, zero_code);
-      if (__float_as_uint(a0) >= 0x7f800000u || (full && __float_as_uint(a1) >= 0x7f800000u))
-        bad |= MRFP4_STATUS_NONFINITE;
-      if (s0.code == 0 || (full && s1.code == 0)) bad |= MRFP4_STATUS_SCALE_UNDERFLOW;
-      sfc = s0.code | (full ? s1.code << 8 : 0u);
-    } else {
-      const float a = max3n(a0, a1, 0.f);
-      if (__float_as_uint(a) >= 0x7f800000u) bad |= MRFP4_STATUS_NONFINITE;
-      s0 = mx_group_scale(a, p);
-      s1 = s0;
-      sfc = s0.code;
-    }
-    uint32_t w[4];
-    quantize_seg(P, s0, s1, st32, p, w);
-
-    uint8_t* cdst = p.codes + (uint64_t)c.row * p.half_k + (uint32_t)(col0 >> 1);
-    if (full) {
-      if ((p.Ki & 31) == 0) {
-        *reinterpret_cast<uint4*>(cdst) = make_uint4(w[0], w[1], w[2], w[3]);
-      } else {
-        reinterpret_cast<uint2*>(cdst)[0] = make_uint2(w[0], w[1]);
-        reinterpret_cast<uint2*>(cdst)[1] = make_uint2(w[2], w[3]);
-      }
-    } else {
-      *reinterpret_cast<uint2*>(cdst) = make_uint2(w[0], w[1]);
-    }
-    if constexpr (FMT == MRFP4_FMT_MXFP4) {
-      p.sf[sf_off32(c.row, c.seg, p.cb)] = (uint8_t)sfc;
-    } else {
-      // columns 2*seg, 2*seg+1 share a 16-bit word of the swizzled layout
-      *reinterpret_cast<uint16_t*>(p.sf + sf_off32(c.row, 2 * c.seg, p.cb)) = (uint16_t)sfc;
-    }
+    encode_seg<MRFP4_FMT_MXFP4>(p, c, P, k, bad);
   });
   if (bad) atomic_or_status(p.status, bad);
   zero_sf_padding(p);
-  if constexpr (FMT == MRFP4_FMT_NVFP4) {
-    // Last CTA out re-arms the workspace (gmax = 0, counter = 0) for the next call:
-    // every CTA read gmax before it arrives here.
-    __syncthreads();
-    if (threadIdx.x == 0) {
+}
+
+// NVFP4: the whole-tensor scale (quantizers.py:198-200) must be known before any group is
+// encoded.  One persistent launch: phase 1 streams X and reduces max |y| into gmax, a
+// grid barrier (all CTAs are co-resident by construction), then phase 2 walks each warp's
+// items BACKWARDS -- the last kStages items of every lane are still in its SMEM ring, the
+// rest are re-read (mostly L2 hits).  Workspace words: [0] gmax, [1] barrier count,
+// [2] barrier generation, [3] exit count; the last CTA out re-zeroes [0], [3].
+template <int IN, int HK>
+__global__ void __launch_bounds__(kThreads, 3) k_act_quant_nv(AQParams p) {
+  using C = InCfg<IN>;
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t* ws = p.gmax;
+  volatile uint32_t* vgen = ws + 2;
+  const uint32_t gen0 = *vgen;  // before arriving: the barrier releases when gen != gen0
+
+  // ---- phase 1: max |y| over the tensor
+  float m = 0.f;
+  for_each_seg<IN, 1, false>(p, [] {}, [&](const Cursor&, uint32_t sbase) {
+    u64 P[kPairs];
+    load_pairs<IN>(sbase, lane, P);
+    if constexpr (HK > 0) fwht<HK>(P, lane, p.pm);
+    float a, b;
+    half_amax(P, a, b);   // padding rows / columns were zero-filled
+    m = max3n(a, b, m);
+  });
+  uint32_t mb = __float_as_uint(m);
+  mb = mb > 0x7f800000u ? 0x7fc00000u : mb;  // canonical NaN
+  mb = __reduce_max_sync(0xffffffffu, mb);
+  __shared__ uint32_t smax[kWarps];
+  __shared__ uint32_t sg;
+  if (lane == 0) smax[warp] = mb;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t x = 0;
+    for (int i = 0; i < kWarps; ++i) x = max(x, smax[i]);
+    if (x) atomicMax(ws, x);
+    if (x >= 0x7f800000u) atomic_or_status(p.status, MRFP4_STATUS_NONFINITE);
+    // ---- grid barrier
+    __threadfence();
+    if (atomicAdd(ws + 1, 1u) == gridDim.x - 1) {
+      ws[1] = 0u;
       __threadfence();
-      if (atomicAdd(p.gmax + 1, 1u) == gridDim.x - 1) {
-        p.gmax[0] = 0u;
-        p.gmax[1] = 0u;
-        __threadfence();
+      atomicAdd(ws + 2, 1u);
+    } else {
+      while (*vgen == gen0) __nanosleep(64);
+    }
+    __threadfence();
+    sg = *(volatile uint32_t*)ws;
+  }
+  __syncthreads();
+  pdl_trigger();  // only after the barrier: every CTA of this grid is resident by now
+  const EncConsts k = nv_consts(p, sg);
+  if (blockIdx.x == 0 && threadIdx.x == 0) *p.tensor_scale = k.st32;
+
+  // ---- phase 2: encode, backwards over this warp's items
+  uint32_t bad = 0;
+  const int64_t gw = (int64_t)blockIdx.x * kWarps + warp, tw = (int64_t)gridDim.x * kWarps;
+  const int64_t i0 = gw * p.items / tw, i1 = (gw + 1) * p.items / tw;
+  const int n = (int)(i1 - i0);
+  if (n > 0) {
+    const uint32_t base =
+        (uint32_t)__cvta_generic_to_shared(smem_raw) + (uint32_t)((warp * kStages * 32 + lane) * C::kLaneBytes);
+    constexpr uint32_t kStride = 32 * C::kLaneBytes;
+    Cursor cp = cursor_at(p, i1 - 1, lane);                    // item n-1 (phase-1 slot (n-1) % kStages)
+    Cursor cr = cp;                                            // reload cursor: item n-1-kStages
+    for (int t = 0; t < kStages; ++t) cursor_step<-1>(p, cr);
+    for (int kk = n - 1; kk >= 0; --kk) {
+      const uint32_t slot = base + (uint32_t)(kk % kStages) * kStride;
+      if (kk < n - kStages) cp_wait<kStages - 1>();           // item kk's reload landed
+      u64 P[kPairs];
+      load_pairs<IN>(slot, lane, P);
+      if constexpr (HK > 0) fwht<HK>(P, lane, p.pm);
+      encode_seg<MRFP4_FMT_NVFP4>(p, cp, P, k, bad);
+      if (kk - kStages >= 0) {                                 // refill this slot with item kk - kStages
+        issue_seg<IN>(p, cr, slot, lane);
+        cursor_step<-1>(p, cr);
       }
+      cp_commit();
+      cursor_step<-1>(p, cp);
+    }
+    cp_wait<0>();
+  }
+  if (bad) atomic_or_status(p.status, bad);
+  zero_sf_padding(p);
+  // Last CTA out re-arms gmax for the next call (every CTA read it before the barrier released).
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(ws + 3, 1u) == gridDim.x - 1) {
+      ws[0] = 0u;
+      ws[3] = 0u;
+      __threadfence();
     }
   }
 }
@@ -681,11 +747,8 @@ int launch_persistent(int smem, const AQParams& p, cudaStream_t s) {
 template <int IN, int FMT, int HK>
 int launch_hk(const AQParams& p, cudaStream_t s) {
   constexpr int smem = InCfg<IN>::kSmem;
-  if constexpr (FMT == MRFP4_FMT_NVFP4) {
-    const int rc = launch_persistent<k_tensor_absmax<IN, HK>>(smem, p, s);
-    if (rc != MRFP4_OK) return rc;
-  }
-  return launch_persistent<k_act_quant<IN, FMT, HK>>(smem, p, s);
+  if constexpr (FMT == MRFP4_FMT_NVFP4) return launch_persistent<k_act_quant_nv<IN, HK>>(smem, p, s);
+  return launch_persistent<k_act_quant_mx<IN, HK>>(smem, p, s);
 }
 
 template <int IN, int FMT>

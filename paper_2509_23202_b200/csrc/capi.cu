@@ -14,7 +14,8 @@ int launch_act_quant(const void* x, int x_dtype, int64_t M, int64_t K, int64_t l
                      uint8_t* sf, float* tensor_scale, uint32_t* status, void* workspace, cudaStream_t s);
 int launch_gemm_fp4(const uint8_t* a, const uint8_t* a_sf, const float* a_ts, const uint8_t* b, const uint8_t* b_sf,
                     const float* b_ts, void* d, int d_dtype, int64_t M, int64_t N, int64_t K, int64_t ldd, int fmt,
-                    cudaStream_t s);
+                    void* ws, size_t ws_bytes, cudaStream_t s);
+size_t gemm_workspace_bytes(int64_t M, int64_t N, int64_t K);
 int launch_sf_swizzle(const uint8_t* src, uint8_t* dst, int64_t rows, int64_t cols, cudaStream_t s);
 int launch_sf_unswizzle(const uint8_t* src, uint8_t* dst, int64_t rows, int64_t cols, cudaStream_t s);
 int launch_dequantize(const uint8_t* codes, const uint8_t* sf, const float* ts, int64_t rows, int64_t cols, int fmt,
@@ -94,8 +95,8 @@ int mrfp4_act_quant(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ld
   if (((uint64_t)ldx * es) % 16 || !aligned(x, 16))
     return fail(MRFP4_EUNSUPPORTED, "input rows must be 16-byte aligned");
   if (!aligned(codes, 16) || !aligned(sf, 2)) return fail(MRFP4_EUNSUPPORTED, "output buffers must be 16-byte aligned");
-  if (fmt == MRFP4_FMT_NVFP4 && (workspace == nullptr || workspace_bytes < 8 || !aligned(workspace, 4)))
-    return fail(MRFP4_EINVAL, "NVFP4 needs an 8-byte, 4-byte aligned, zero-initialised device workspace");
+  if (fmt == MRFP4_FMT_NVFP4 && (workspace == nullptr || workspace_bytes < 16 || !aligned(workspace, 4)))
+    return fail(MRFP4_EINVAL, "NVFP4 needs a 16-byte, 4-byte aligned, zero-initialised device workspace");
   const int rc = mrfp4::launch_act_quant(x, x_dtype, M, K, ldx, fmt, had_k, codes, sf, tensor_scale, status,
                                          workspace, static_cast<cudaStream_t>(stream));
   return cuda_status(rc, "mrfp4_act_quant");
@@ -113,9 +114,14 @@ int mrfp4_sf_unswizzle(const uint8_t* src, uint8_t* dst, int64_t rows, int64_t c
                      "mrfp4_sf_unswizzle");
 }
 
+size_t mrfp4_gemm_workspace(int64_t M, int64_t N, int64_t K, int fmt) {
+  if (mrfp4_group_size(fmt) == 0 || M < 1 || N < 1 || K < 1) return 0;
+  return mrfp4::gemm_workspace_bytes(M, N, K);
+}
+
 int mrfp4_gemm(const uint8_t* a, const uint8_t* a_sf, const float* a_ts, const uint8_t* b, const uint8_t* b_sf,
                const float* b_ts, void* d, int d_dtype, int64_t M, int64_t N, int64_t K, int64_t ldd, int fmt,
-               void* stream) {
+               void* workspace, size_t workspace_bytes, void* stream) {
   if (mrfp4_group_size(fmt) == 0) return fail(MRFP4_EUNSUPPORTED, "unknown format %d", fmt);
   if (d_dtype != MRFP4_DT_BF16 && d_dtype != MRFP4_DT_F32)
     return fail(MRFP4_EUNSUPPORTED, "output dtype must be bf16 or f32");
@@ -127,8 +133,9 @@ int mrfp4_gemm(const uint8_t* a, const uint8_t* a_sf, const float* a_ts, const u
   if (!aligned(a, 16) || !aligned(b, 16) || !aligned(a_sf, 16) || !aligned(b_sf, 16) || !aligned(d, 16) ||
       (ldd * elt_size(d_dtype)) % 16)
     return fail(MRFP4_EUNSUPPORTED, "GEMM buffers must be 16-byte aligned");
-  const int rc = mrfp4::launch_gemm_fp4(a, a_sf, a_ts, b, b_sf, b_ts, d, d_dtype, M, N, K, ldd, fmt,
-                                        static_cast<cudaStream_t>(stream));
+  if (workspace && !aligned(workspace, 16)) return fail(MRFP4_EINVAL, "GEMM workspace must be 16-byte aligned");
+  const int rc = mrfp4::launch_gemm_fp4(a, a_sf, a_ts, b, b_sf, b_ts, d, d_dtype, M, N, K, ldd, fmt, workspace,
+                                        workspace ? workspace_bytes : 0, static_cast<cudaStream_t>(stream));
   return cuda_status(rc, "mrfp4_gemm");
 }
 

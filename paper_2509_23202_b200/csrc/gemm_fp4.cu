@@ -70,6 +70,10 @@ struct GemmArgs {
   int64_t b_row_blocks;   // ceil(N / 128)
   int num_m_blk, num_n_blk, num_kb;
   int tail_mmas;  // MMAs in the last k-block (0 = full)
+  int splits;     // 1-CTA kernel: K splits per output tile (> 1: fp32 partials to `ws`)
+  int kb_per;     // k-blocks per split
+  float* ws;      // [splits][M][N] fp32 partial sums (splits > 1)
+  size_t ws_bytes;
   unsigned long long* dbg;  // perf experiments: per-k-block MMA-thread timestamps of CTA 0
   int debug;  // perf experiments: 1 = no operand loads, 2 = no MMAs (0 in production)
 };
@@ -209,7 +213,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem_base = *tmem_holder;
   pdl_trigger();
 
-  const int num_tiles = g.num_m_blk * g.num_n_blk;
+  const int num_units = g.num_m_blk * g.num_n_blk * g.splits;
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
@@ -217,9 +221,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       pdl_wait();  // A, its scale factors and tensor scale come from the act-quant kernel
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      for (int unit = blockIdx.x; unit < num_units; unit += gridDim.x) {
+        const int tile = unit / g.splits, split = unit - tile * g.splits;
         const int m_blk = tile % g.num_m_blk, n_blk = tile / g.num_m_blk;
-        for (int kb = 0; kb < g.num_kb; ++kb) {
+        const int kb0 = split * g.kb_per, kb1 = min(g.num_kb, kb0 + g.kb_per);
+        for (int kb = kb0; kb < kb1; ++kb) {
           sm100::mbar_wait(&empty[stage], phase ^ 1);
           const int atoms = (int)imin64(C::kAtomsPerKb, g.sf_col_blocks - (int64_t)kb * C::kAtomsPerKb);
           int nbv = 0;
@@ -255,13 +261,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0, acc_phase = 0;
       const uint64_t adesc0 = sm100::smem_desc(sm100::smem_u32(smem + C::kOffA), 16, 1024, 2);
       const uint64_t bdesc0 = sm100::smem_desc(sm100::smem_u32(smem + C::kOffB), 16, 1024, 2);
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      for (int unit = blockIdx.x; unit < num_units; unit += gridDim.x) {
+        const int split = unit % g.splits;
+        const int kb0 = split * g.kb_per, kb1 = min(g.num_kb, kb0 + g.kb_per);
         sm100::mbar_wait(tempty, acc_phase ^ 1);
         sm100::tc_fence_after();
-        for (int kb = 0; kb < g.num_kb; ++kb) {
-          if (g.dbg && blockIdx.x == 0 && tile == 0 && kb < 64) g.dbg[2 * kb] = clock64();
+        for (int kb = kb0; kb < kb1; ++kb) {
           sm100::mbar_wait(&full[stage], phase);
-          if (g.dbg && blockIdx.x == 0 && tile == 0 && kb < 64) g.dbg[2 * kb + 1] = clock64();
           sm100::tc_fence_after();
           const uint32_t sfa_t = tmem_base + C::kAccCols + stage * (C::kSfaCols + C::kSfbCols);
           const uint32_t sfb_t = sfa_t + C::kSfaCols;
@@ -281,9 +287,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint64_t bd = desc_add(bdesc0, (uint32_t)(stage * (C::kBBytes >> 4)));
           if (g.debug == 2 || g.debug == 4) {
           } else if (kb + 1 < g.num_kb || g.tail_mmas == 0) {
-            issue_kblock<VEC, BK / UMMA_K, BM, BN, C::kNB, false>(tmem_base, ad, bd, sfa_t, sfb_t, kb == 0);
+            issue_kblock<VEC, BK / UMMA_K, BM, BN, C::kNB, false>(tmem_base, ad, bd, sfa_t, sfb_t, kb == kb0);
           } else {
-            issue_kblock_any<VEC, BM, BN, C::kNB, false>(g.tail_mmas, tmem_base, ad, bd, sfa_t, sfb_t, kb == 0);
+            issue_kblock_any<VEC, BM, BN, C::kNB, false>(g.tail_mmas, tmem_base, ad, bd, sfa_t, sfb_t, kb == kb0);
           }
           sm100::tc_commit(&empty[stage]);
           if (++stage == C::kStages) { stage = 0; phase ^= 1; }
@@ -298,18 +304,33 @@ __global__ void __launch_bounds__(kThreads, 1)
     pdl_wait();
     const float alpha = __ldg(g.a_ts) * __ldg(g.b_ts);
     uint32_t acc_phase = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+    for (int unit = blockIdx.x; unit < num_units; unit += gridDim.x) {
+      const int tile = unit / g.splits, split = unit - tile * g.splits;
       const int m_blk = tile % g.num_m_blk, n_blk = tile / g.num_m_blk;
       sm100::mbar_wait(tfull, acc_phase);
       sm100::tc_fence_after();
       const int64_t row = (int64_t)m_blk * BM + q * 32 + lane;
+      // Split-K: lanes past M skip the TMEM read entirely when the whole warp is past M.
+      const bool warp_live = (int64_t)m_blk * BM + q * 32 < g.M;
 #pragma unroll 1
-      for (int c = 0; c < ((g.debug >= 3 && g.debug <= 5) ? 0 : BN); c += 32) {
+      for (int c = 0; c < ((g.debug >= 3 && g.debug <= 5) || !warp_live ? 0 : BN); c += 32) {
         uint32_t r[32];
         sm100::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + c, r);
         sm100::tmem_ld_wait();
         const int64_t col = (int64_t)n_blk * BN + c;
-        if (row < g.M) store_row32<OUT>(g, row, col, r, alpha);
+        if (row < g.M) {
+          if (g.splits == 1) {
+            store_row32<OUT>(g, row, col, r, alpha);
+          } else {  // fp32 partial, unscaled: ws[split][row][col]
+            float* dst = g.ws + ((int64_t)split * g.M + row) * g.N + col;
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              if (col + 4 * j < g.N)
+                *reinterpret_cast<float4*>(dst + 4 * j) =
+                    make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]), __uint_as_float(r[4 * j + 2]),
+                                __uint_as_float(r[4 * j + 3]));
+          }
+        }
       }
       sm100::tc_fence_before();
       __syncwarp();
@@ -324,6 +345,33 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+
+// Split-K reduction: d[m, n] = ts_A * ts_W * sum_s ws[s][m][n] (fixed order: deterministic).
+template <int OUT>
+__global__ void __launch_bounds__(256) k_splitk_reduce(const float* __restrict__ ws, int splits, const float* a_ts,
+                                                       const float* b_ts, void* d, int64_t M, int64_t N, int64_t ldd) {
+  pdl_wait();
+  pdl_trigger();
+  const float alpha = __ldg(a_ts) * __ldg(b_ts);
+  const int64_t n4 = N / 4, total = M * n4;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t m = i / n4, c = (i - m * n4) * 4;
+    float4 acc = *reinterpret_cast<const float4*>(ws + m * N + c);
+    for (int s = 1; s < splits; ++s) {
+      const float4 v = *reinterpret_cast<const float4*>(ws + ((int64_t)s * M + m) * N + c);
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+    if constexpr (OUT == MRFP4_DT_BF16) {
+      __nv_bfloat162 lo = __floats2bfloat162_rn(acc.x * alpha, acc.y * alpha);
+      __nv_bfloat162 hi = __floats2bfloat162_rn(acc.z * alpha, acc.w * alpha);
+      *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(d) + m * ldd + c) =
+          make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+    } else {
+      *reinterpret_cast<float4*>(static_cast<float*>(d) + m * ldd + c) =
+          make_float4(acc.x * alpha, acc.y * alpha, acc.z * alpha, acc.w * alpha);
+    }
+  }
+}
 
 // ---------------------------------------------------------------------------
 // 2-CTA (cta_group::2) kernel: a CTA pair computes a 256 x 256 output tile, persistent
@@ -712,6 +760,10 @@ bool make_code_map3(CUtensorMap* tm, const uint8_t* ptr, int64_t rows, int64_t K
   return r == CUDA_SUCCESS;
 }
 
+// Split-K plan for `tiles` output tiles of `num_kb` k-blocks: about one unit per SM, at
+// least 2 k-blocks per split.
+void splitk_plan(int tiles, int num_kb, int* splits, int* kb_per);
+
 int num_sms() {
   static int n = 0;
   if (n == 0) {
@@ -743,11 +795,30 @@ int launch(const uint8_t* a, const uint8_t* b, const GemmArgs& args0, cudaStream
   g.sf_col_blocks = ceil_div(g.K / VEC, 4);
   g.b_row_blocks = ceil_div(g.N, 128);
   const int tiles = g.num_m_blk * g.num_n_blk;
-  int grid = std::min(tiles, num_sms());
+  // Small M (weight-bandwidth bound): split K so every SM streams a slice of the weight.
+  g.splits = 1;
+  g.kb_per = g.num_kb;
+  if (g.ws) {
+    int sp = 1, per = g.num_kb;
+    splitk_plan(tiles, g.num_kb, &sp, &per);
+    if (sp > 1 && g.ws_bytes >= (size_t)sp * g.M * g.N * sizeof(float)) {
+      g.splits = sp;
+      g.kb_per = per;
+    }
+  }
+  const int units = tiles * g.splits;
+  int grid = std::min(units, num_sms());
   if (g_force_grid > 0) grid = std::min(grid, g_force_grid);
-  return launch_pdl(k_gemm_fp4<VEC, BN, OUT>, dim3(grid), dim3(kThreads), C::kSmem, s, tmA, tmB, g) == cudaSuccess
-             ? MRFP4_OK
-             : MRFP4_ECUDA;
+  if (launch_pdl(k_gemm_fp4<VEC, BN, OUT>, dim3(grid), dim3(kThreads), C::kSmem, s, tmA, tmB, g) != cudaSuccess)
+    return MRFP4_ECUDA;
+  if (g.splits > 1) {
+    const int64_t work = g.M * (g.N / 4);
+    const int rgrid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(work, 256), 4 * num_sms()));
+    if (launch_pdl(k_splitk_reduce<OUT>, dim3(rgrid), dim3(256), 0, s, (const float*)g.ws, g.splits, g.a_ts, g.b_ts,
+                   g.d, g.M, g.N, g.ldd) != cudaSuccess)
+      return MRFP4_ECUDA;
+  }
+  return MRFP4_OK;
 }
 
 template <int VEC, int OUT>
@@ -781,7 +852,25 @@ int launch2(const uint8_t* a, const uint8_t* b, const GemmArgs& args0, cudaStrea
              : MRFP4_ECUDA;
 }
 
+void splitk_plan(int tiles, int num_kb, int* splits, int* kb_per) {
+  int sp = 1;
+  if (tiles * 2 <= num_sms()) sp = std::min(std::max(1, num_sms() / tiles), std::max(1, num_kb / 2));
+  const int per = (int)ceil_div(num_kb, sp);
+  *kb_per = per;
+  *splits = (int)ceil_div(num_kb, per);
+}
+
 }  // namespace
+
+// Workspace bytes mrfp4_gemm uses for split-K at this shape (0 when it does not split).
+size_t gemm_workspace_bytes(int64_t M, int64_t N, int64_t K) {
+  const bool pair = (K % 256 == 0) && M > 128;
+  if (pair) return 0;
+  const int tiles = (int)(ceil_div(M, BM) * ceil_div(N, 256));
+  int sp = 1, per = 1;
+  splitk_plan(tiles, (int)ceil_div(K, BK), &sp, &per);
+  return sp > 1 ? (size_t)sp * M * N * sizeof(float) : 0;
+}
 
 int g_debug_mode = 0;
 unsigned long long* g_debug_buf = nullptr;
@@ -790,8 +879,10 @@ int g_force_kernel = 0;  // 0 auto, 1 = 1-CTA kernel, 2 = 2-CTA kernel
 
 int launch_gemm_fp4(const uint8_t* a, const uint8_t* a_sf, const float* a_ts, const uint8_t* b, const uint8_t* b_sf,
                     const float* b_ts, void* d, int d_dtype, int64_t M, int64_t N, int64_t K, int64_t ldd, int fmt,
-                    cudaStream_t s) {
+                    void* ws, size_t ws_bytes, cudaStream_t s) {
   GemmArgs g{};
+  g.ws = static_cast<float*>(ws);
+  g.ws_bytes = ws_bytes;
   g.debug = g_debug_mode;
   g.dbg = g_debug_buf;
   g.a_sf = a_sf;

@@ -125,15 +125,34 @@ def quantize_weight(W, spec, transform=None, *, check: bool = True) -> PackedWei
     return prepare_weight(quantize_rtn(W, spec, transform=transform, check=check))
 
 
+_WORKSPACE: dict = {}
+
+
+def _gemm_workspace(device: torch.device, stream: int, nbytes: int):
+    """Split-K scratch, one growing buffer per (device, stream) so stream-ordered reuse is safe."""
+    if nbytes == 0:
+        return None
+    key = (device.index, stream)
+    buf = _WORKSPACE.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        _WORKSPACE[key] = buf
+    return buf
+
+
 def gemm(a: GpuQuantResult, w: PackedWeight, out: torch.Tensor) -> torch.Tensor:
     """K2 only: out[M, N] = a . w^T with both operands already quantized."""
     if a.fmt != w.fmt or a.cols != w.K:
         raise DataError("activation / weight format or K mismatch")
-    _lib.check(_lib.lib().mrfp4_gemm(
+    L = _lib.lib()
+    stream = _lib.stream_ptr(torch, out.device)
+    nbytes = L.mrfp4_gemm_workspace(a.rows, w.N, w.K, w.fmt)
+    ws = _gemm_workspace(out.device, stream, nbytes)
+    _lib.check(L.mrfp4_gemm(
         _lib.ptr(a.codes), _lib.ptr(a.sf), _lib.ptr(a.tensor_scale_dev),
         _lib.ptr(w.codes), _lib.ptr(w.sf), _lib.ptr(w.tensor_scale_dev),
         _lib.ptr(out), _OUT[out.dtype], a.rows, w.N, w.K, out.stride(0), w.fmt,
-        _lib.stream_ptr(torch, out.device)))
+        _lib.ptr(ws), nbytes, stream))
     return out
 
 

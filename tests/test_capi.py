@@ -26,7 +26,15 @@ def test_library_exports_every_symbol():
     L = _lib.lib()
     for name in header_symbols():
         assert hasattr(L, name), name
-    assert L.mrfp4_abi_version() == 1
+    assert L.mrfp4_abi_version() == 2
+
+
+def test_gemm_workspace_sizes():
+    L = _lib.lib()
+    assert L.mrfp4_gemm_workspace(2048, 4096, 14336, 0) == 0          # 2-CTA path: no split
+    ws = L.mrfp4_gemm_workspace(16, 4096, 4096, 1)                     # C0 decode shape: split-K
+    assert ws > 0 and ws % (16 * 4096 * 4) == 0
+    assert L.mrfp4_gemm_workspace(16, 4096, 4096, 9) == 0             # unknown format
 
 
 def test_sizes():
@@ -61,11 +69,11 @@ def test_act_quant_argument_errors(args, msg):
 
 def test_gemm_argument_errors():
     L = _lib.lib()
-    rc = L.mrfp4_gemm(16, 16, 16, 16, 16, 16, 16, 0, 128, 256, 96, 256, 0, None)
+    rc = L.mrfp4_gemm(16, 16, 16, 16, 16, 16, 16, 0, 128, 256, 96, 256, 0, None, 0, None)
     assert rc == _lib.EUNSUPPORTED and "multiple of 64" in L.mrfp4_last_error().decode()
-    rc = L.mrfp4_gemm(16, 16, 16, 16, 16, 16, 16, 0, 128, 250, 128, 256, 0, None)
+    rc = L.mrfp4_gemm(16, 16, 16, 16, 16, 16, 16, 0, 128, 250, 128, 256, 0, None, 0, None)
     assert rc == _lib.EUNSUPPORTED and "multiple of 8" in L.mrfp4_last_error().decode()
-    rc = L.mrfp4_gemm(16, 16, 16, 16, 16, 16, 16, 5, 128, 256, 128, 256, 0, None)
+    rc = L.mrfp4_gemm(16, 16, 16, 16, 16, 16, 16, 5, 128, 256, 128, 256, 0, None, 0, None)
     assert rc == _lib.EUNSUPPORTED
 
 

@@ -82,6 +82,24 @@ def test_gemm_random_codes_fp32(fmt, M, N, K, kernel):
 
 
 @pytest.mark.parametrize("fmt", ["mxfp4", "nvfp4"])
+@pytest.mark.parametrize("M,N,K,dtype", [
+    (16, 4096, 4096, torch.float32), (16, 4096, 4096, torch.bfloat16), (1, 512, 2048, torch.float32),
+    (100, 1024, 8192, torch.float32), (128, 2048, 5120, torch.bfloat16), (7, 264, 1856, torch.float32)])
+def test_gemm_small_m_split_k(fmt, M, N, K, dtype):
+    """Small-M (decode) shapes take the split-K path: fp32 partials per K slice, reduced in a
+    fixed order by a second kernel -- same result as the unsplit GEMM."""
+    from paper_2509_23202_b200 import _lib
+    assert _lib.lib().mrfp4_gemm_workspace(M, N, K, 0 if fmt == "mxfp4" else 1) > 0 or N >= 256 * 74
+    rng = np.random.default_rng(M * 17 + N + K)
+    A, W = random_container(rng, M, K, fmt), random_container(rng, N, K, fmt)
+    y = run_gemm(A, W, dtype).float().cpu().numpy()
+    ref = ref64(A, W)
+    assert rel_fro(y, ref) <= (1e-5 if dtype == torch.float32 else 3e-3), rel_fro(y, ref)
+    y2 = run_gemm(A, W, dtype).float().cpu().numpy()
+    assert np.array_equal(y, y2)   # deterministic reduction order
+
+
+@pytest.mark.parametrize("fmt", ["mxfp4", "nvfp4"])
 def test_gemm_bf16_output_within_one_ulp(fmt):
     rng = np.random.default_rng(5)
     A, W = random_container(rng, 256, 1024, fmt), random_container(rng, 512, 1024, fmt)
