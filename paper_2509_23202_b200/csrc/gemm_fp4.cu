@@ -150,6 +150,13 @@ __device__ __forceinline__ void issue_kblock_any(int nk, uint32_t d_tmem, uint64
   }
 }
 
+// 256-bit global store (sm_100): 8 words to a 32-byte aligned address.
+__device__ __forceinline__ void st_global_v8(void* p, const uint32_t* r) {
+  asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(r[0]), "r"(r[1]), "r"(r[2]),
+               "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
+}
+
 // 32 consecutive accumulator columns of one output row -> global (bf16 or f32).
 template <int OUT>
 __device__ __forceinline__ void store_row32(const GemmArgs& g, int64_t row, int64_t col, const uint32_t (&r)[32],
@@ -578,10 +585,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(448, 1)
       const uint64_t adesc0 = sm100::smem_desc(sm100::smem_u32(smem + C::kOffA), 16, 1024, 2);
       const uint64_t bdesc0 = sm100::smem_desc(sm100::smem_u32(smem + C::kOffB), 16, 1024, 2);
       const uint32_t sf0 = tmem_base + C::kAccCols;
-      for (int tile = cluster; tile < num_tiles; tile += nclusters) {
+      unsigned long long* dbg = (g.dbg && cluster == 0) ? g.dbg : nullptr;  // perf traces (tests pass null)
+      int ntl = 0;
+      for (int tile = cluster; tile < num_tiles; tile += nclusters, ++ntl) {
+        if (dbg && ntl < 4) dbg[ntl * 260] = clock64();
         sm100::mbar_wait(tempty, acc_phase ^ 1);
+        if (dbg && ntl < 4) dbg[ntl * 260 + 1] = clock64();
         for (int kb = 0; kb < num_kb; ++kb) {
           sm100::mbar_wait(&full[ab.idx], ab.ph);
+          if (dbg && ntl < 4 && kb < 128) dbg[ntl * 260 + 2 + 2 * kb] = clock64();
           sm100::tc_fence_after();
           const uint32_t sfa_t = sf0 + sf.idx * C::kSfCols, sfb_t = sfa_t + C::kSfaCols;
           const uint64_t ad = desc_add(adesc0, (uint32_t)(ab.idx * (C::kABytes >> 4)));
@@ -592,6 +604,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(448, 1)
             issue_stage_tail<VEC>(tail_mmas, el, tmem_base, ad, bd, sfa_t, sfb_t, kb == 0);
           sm100::tc_commit_2sm_mc_if(el, &empty[ab.idx], 0x3);
           sm100::tc_commit_2sm_mc_if(el, &tsf_empty[sf.idx], 0x3);
+          if (dbg && ntl < 4 && kb < 128) dbg[ntl * 260 + 3 + 2 * kb] = clock64();
           ab.next<C::kStages>();
           sf.next<C::kSfSlots>();
         }
@@ -682,10 +695,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(448, 1)
         }
         if (row < g.M) {
           __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(g.d) + row * g.ldd + col0;
+          // 32-B stores: whole L2 sectors per lane (16-B stores from 32 rows at once were
+          // partial-sector writes that stalled the next tile's pipeline by ~5K cycles).
+          if ((g.ldd & 15) == 0 && col0 + 128 <= g.N) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j)
-            if (col0 + 8 * j < g.N)
-              *reinterpret_cast<uint4*>(dst + 8 * j) = make_uint4(pkd[4 * j], pkd[4 * j + 1], pkd[4 * j + 2], pkd[4 * j + 3]);
+            for (int j = 0; j < 8; ++j) st_global_v8(dst + 16 * j, pkd + 8 * j);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (col0 + 8 * j < g.N)
+                *reinterpret_cast<uint4*>(dst + 8 * j) = make_uint4(pkd[4 * j], pkd[4 * j + 1], pkd[4 * j + 2], pkd[4 * j + 3]);
+          }
         }
       } else {
 #pragma unroll 1
