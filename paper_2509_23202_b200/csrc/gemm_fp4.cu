@@ -60,6 +60,7 @@ struct Cfg {
 __host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
 
 struct GemmArgs {
+  const uint8_t* b;       // weight codes [N, K/2] (L2 prefetch of upcoming panels)
   const uint8_t* a_sf;
   const uint8_t* b_sf;
   const float* a_ts;
@@ -474,6 +475,27 @@ __device__ __forceinline__ void issue_stage_tail(int nk, uint32_t el, uint32_t d
   }
 }
 
+// Work of one cluster, identical for all roles of both CTAs: whole 256 x 256 tiles,
+// tile = cluster + i * clusters (m-block fastest, so concurrent pairs share weight panels in L2).
+// (A stream-K tail -- splitting a sparse last wave's k-stages across pairs with fp32
+// partials -- was implemented and measured slower than this schedule in every case tried on
+// B200, e.g. 256x14336x8192: 46.0 vs 34.9 us, and removed.)
+struct Work {
+  int tile, kb0, kb1;
+};
+
+struct WorkIter {
+  int c, C, i;
+  __device__ __forceinline__ WorkIter(const GemmArgs&, int cluster, int nclusters) : c(cluster), C(nclusters), i(0) {}
+  __device__ __forceinline__ bool next(const GemmArgs& g, Work& w) {
+    const int t = c + i * C;
+    if (t >= g.num_m_blk * g.num_n_blk) return false;
+    ++i;
+    w = Work{t, 0, g.num_kb};
+    return true;
+  }
+};
+
 // Ring position: slot index and parity, advanced once per stage.
 struct Ring {
   int idx = 0;
@@ -503,8 +525,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(448, 1)
   const bool leader = rank == 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // Kernel parameters into registers once (asm "memory" clobbers would force reloads).
-  const int num_m_blk = g.num_m_blk, num_n_blk = g.num_n_blk, num_kb = g.num_kb, tail_mmas = g.tail_mmas;
-  const int num_tiles = num_m_blk * num_n_blk;
+  const int num_m_blk = g.num_m_blk, num_kb = g.num_kb, tail_mmas = g.tail_mmas;
   const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
   const int64_t sf_col_blocks = g.sf_col_blocks, b_row_blocks = g.b_row_blocks, a_row_blocks = (g.M + 127) / 128;
 
@@ -537,9 +558,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(448, 1)
       // ------------------------------------------------------------- producer
       pdl_wait();  // A, its scale factors and tensor scale come from the act-quant kernel
       Ring ab, sf;
-      for (int tile = cluster; tile < num_tiles; tile += nclusters) {
-        const int m_blk = tile % num_m_blk, n_blk = tile / num_m_blk;
-        for (int kb = 0; kb < num_kb; ++kb) {
+      WorkIter it(g, cluster, nclusters);
+      Work w;
+      while (it.next(g, w)) {
+        const int m_blk = w.tile % num_m_blk, n_blk = w.tile / num_m_blk;
+        for (int kb = w.kb0; kb < w.kb1; ++kb) {
           sm100::mbar_wait(&sf_empty[sf.idx], sf.ph ^ 1);
           {
             // Scale factors: contiguous 512-B atoms per 128-row block -> 1-D bulk copies
@@ -587,24 +610,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(448, 1)
       const uint32_t sf0 = tmem_base + C::kAccCols;
       unsigned long long* dbg = (g.dbg && cluster == 0) ? g.dbg : nullptr;  // perf traces (tests pass null)
       int ntl = 0;
-      for (int tile = cluster; tile < num_tiles; tile += nclusters, ++ntl) {
+      WorkIter it(g, cluster, nclusters);
+      Work w;
+      for (; it.next(g, w); ++ntl) {
         if (dbg && ntl < 4) dbg[ntl * 260] = clock64();
         sm100::mbar_wait(tempty, acc_phase ^ 1);
         if (dbg && ntl < 4) dbg[ntl * 260 + 1] = clock64();
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kb = w.kb0; kb < w.kb1; ++kb) {
           sm100::mbar_wait(&full[ab.idx], ab.ph);
-          if (dbg && ntl < 4 && kb < 128) dbg[ntl * 260 + 2 + 2 * kb] = clock64();
+          if (dbg && ntl < 4 && kb - w.kb0 < 128) dbg[ntl * 260 + 2 + 2 * (kb - w.kb0)] = clock64();
           sm100::tc_fence_after();
           const uint32_t sfa_t = sf0 + sf.idx * C::kSfCols, sfb_t = sfa_t + C::kSfaCols;
           const uint64_t ad = desc_add(adesc0, (uint32_t)(ab.idx * (C::kABytes >> 4)));
           const uint64_t bd = desc_add(bdesc0, (uint32_t)(ab.idx * (C::kBBytes >> 4)));
           if (kb + 1 < num_kb || tail_mmas == 0)
-            issue_stage_mmas<VEC, 0, C::kMmas>(el, tmem_base, ad, bd, sfa_t, sfb_t, kb == 0);
+            issue_stage_mmas<VEC, 0, C::kMmas>(el, tmem_base, ad, bd, sfa_t, sfb_t, kb == w.kb0);
           else
-            issue_stage_tail<VEC>(tail_mmas, el, tmem_base, ad, bd, sfa_t, sfb_t, kb == 0);
+            issue_stage_tail<VEC>(tail_mmas, el, tmem_base, ad, bd, sfa_t, sfb_t, kb == w.kb0);
           sm100::tc_commit_2sm_mc_if(el, &empty[ab.idx], 0x3);
           sm100::tc_commit_2sm_mc_if(el, &tsf_empty[sf.idx], 0x3);
-          if (dbg && ntl < 4 && kb < 128) dbg[ntl * 260 + 3 + 2 * kb] = clock64();
+          if (dbg && ntl < 4 && kb - w.kb0 < 128) dbg[ntl * 260 + 3 + 2 * (kb - w.kb0)] = clock64();
           ab.next<C::kStages>();
           sf.next<C::kSfSlots>();
         }
@@ -620,8 +645,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(448, 1)
     const int q = warp & 3;
     Ring ab, sf;
     const uint32_t sa0 = sm100::smem_u32(smem + C::kOffSfa) + lane * 16, sb0 = sm100::smem_u32(smem + C::kOffSfb) + lane * 16;
-    for (int tile = cluster; tile < num_tiles; tile += nclusters) {
-      for (int kb = 0; kb < num_kb; ++kb) {
+    WorkIter it(g, cluster, nclusters);
+    Work w;
+    while (it.next(g, w)) {
+      for (int kb = w.kb0; kb < w.kb1; ++kb) {
         sm100::mbar_wait(&sf_full[sf.idx], sf.ph);
         const uint32_t sa = sa0 + sf.idx * C::kSfaBytes, sb = sb0 + sf.idx * C::kSfbBytes;
         uint32_t ra[C::kSfaCols], rb[C::kSfbCols];
@@ -666,10 +693,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(448, 1)
     pdl_wait();
     const float alpha = __ldg(g.a_ts) * __ldg(g.b_ts);
     uint32_t acc_phase = 0;
-    for (int tile = cluster; tile < num_tiles; tile += nclusters) {
-      const int m_blk = tile % num_m_blk, n_blk = tile / num_m_blk;
+    auto release_acc = [&] {
+      sm100::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (leader) sm100::mbar_arrive(tempty);
+        else sm100::mbar_arrive_remote(tempty, 0);
+      }
+    };
+    WorkIter it(g, cluster, nclusters);
+    Work w;
+    while (it.next(g, w)) {
+      const int m_blk = w.tile % num_m_blk, n_blk = w.tile / num_m_blk;
       sm100::mbar_wait(tfull, acc_phase);
       sm100::tc_fence_after();
+      acc_phase ^= 1;
       const int64_t row = (int64_t)m_blk * 256 + rank * 128 + q * 32 + lane;
       const int64_t col0 = (int64_t)n_blk * 256 + h * 128;
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + h * 128;
@@ -682,17 +720,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(448, 1)
           sm100::tmem_ld_wait();
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
-            __nv_bfloat162 v = __floats2bfloat162_rn(__uint_as_float(r[2 * j]) * alpha,
-                                                     __uint_as_float(r[2 * j + 1]) * alpha);
-            pkd[16 * c + j] = *reinterpret_cast<uint32_t*>(&v);
+            __nv_bfloat162 b2 = __floats2bfloat162_rn(__uint_as_float(r[2 * j]) * alpha, __uint_as_float(r[2 * j + 1]) * alpha);
+            pkd[16 * c + j] = *reinterpret_cast<uint32_t*>(&b2);
           }
         }
-        sm100::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          if (leader) sm100::mbar_arrive(tempty);
-          else sm100::mbar_arrive_remote(tempty, 0);
-        }
+        release_acc();
         if (row < g.M) {
           __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(g.d) + row * g.ldd + col0;
           // 32-B stores: whole L2 sectors per lane (16-B stores from 32 rows at once were
@@ -709,20 +741,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(448, 1)
         }
       } else {
 #pragma unroll 1
-        for (int c = 0; c < 128; c += 32) {
+        for (int c = 0; c < 4; ++c) {
           uint32_t r[32];
-          sm100::tmem_ld_32x32b_x32(taddr + c, r);
+          sm100::tmem_ld_32x32b_x32(taddr + c * 32, r);
           sm100::tmem_ld_wait();
-          if (row < g.M) store_row32<OUT>(g, row, col0 + c, r, alpha);
+          if (row < g.M) store_row32<OUT>(g, row, col0 + c * 32, r, alpha);
         }
-        sm100::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          if (leader) sm100::mbar_arrive(tempty);
-          else sm100::mbar_arrive_remote(tempty, 0);
-        }
+        release_acc();
       }
-      acc_phase ^= 1;
     }
   }
   sm100::tc_fence_before();
@@ -863,8 +889,7 @@ int launch2(const uint8_t* a, const uint8_t* b, const GemmArgs& args0, cudaStrea
   g.sf_col_blocks = ceil_div(sfc, 4);
   g.b_row_blocks = ceil_div(g.N, 128);
   const int tiles = g.num_m_blk * g.num_n_blk;
-  const int clusters = std::min(tiles, num_sms() / 2);
-  int nclu = clusters;
+  int nclu = std::min(tiles, num_sms() / 2);
   if (g_force_grid > 0) nclu = std::min(nclu, std::max(1, g_force_grid / 2));
   return launch_pdl(k_gemm_fp4_2sm<VEC, OUT>, dim3(2 * nclu), dim3(C::kThreads2), C::kSmem, s, tmA, tmB, g) ==
                  cudaSuccess
@@ -885,7 +910,9 @@ void splitk_plan(int tiles, int num_kb, int* splits, int* kb_per) {
 // Workspace bytes mrfp4_gemm uses for split-K at this shape (0 when it does not split).
 size_t gemm_workspace_bytes(int64_t M, int64_t N, int64_t K) {
   const bool pair = (K % 256 == 0) && M > 128;
-  if (pair) return 0;
+  if (pair) {
+    return 0;
+  }
   const int tiles = (int)(ceil_div(M, BM) * ceil_div(N, 256));
   int sp = 1, per = 1;
   splitk_plan(tiles, (int)ceil_div(K, BK), &sp, &per);
@@ -901,6 +928,7 @@ int launch_gemm_fp4(const uint8_t* a, const uint8_t* a_sf, const float* a_ts, co
                     const float* b_ts, void* d, int d_dtype, int64_t M, int64_t N, int64_t K, int64_t ldd, int fmt,
                     void* ws, size_t ws_bytes, cudaStream_t s) {
   GemmArgs g{};
+  g.b = b;
   g.ws = static_cast<float*>(ws);
   g.ws_bytes = ws_bytes;
   g.debug = g_debug_mode;

@@ -129,13 +129,15 @@ _WORKSPACE: dict = {}
 
 
 def _gemm_workspace(device: torch.device, stream: int, nbytes: int):
-    """Split-K scratch, one growing buffer per (device, stream) so stream-ordered reuse is safe."""
+    """GEMM scratch (split-K partials / stream-K flags + partials), one zero-initialised,
+    growing buffer per (device, stream) so stream-ordered reuse is safe (every call leaves
+    the flag words zero again)."""
     if nbytes == 0:
         return None
     key = (device.index, stream)
     buf = _WORKSPACE.get(key)
     if buf is None or buf.numel() < nbytes:
-        buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        buf = torch.zeros(nbytes, dtype=torch.uint8, device=device)  # stream-K flags start at zero
         _WORKSPACE[key] = buf
     return buf
 

@@ -100,6 +100,17 @@ def test_gemm_small_m_split_k(fmt, M, N, K, dtype):
 
 
 @pytest.mark.parametrize("fmt", ["mxfp4", "nvfp4"])
+@pytest.mark.parametrize("M,N,K", [(512, 2048, 4096), (768, 2048, 5120), (300, 1280, 7168), (512, 9728, 4096)])
+def test_gemm_2cta_bf16_shapes(fmt, M, N, K):
+    """2-CTA kernel, bf16 output: ragged M, few tiles, one full wave plus a partial one."""
+    rng = np.random.default_rng(M + N + K)
+    A, W = random_container(rng, M, K, fmt), random_container(rng, N, K, fmt)
+    y = run_gemm(A, W, torch.bfloat16).float().cpu().numpy()
+    assert rel_fro(y, ref64(A, W)) <= 3e-3
+    assert np.array_equal(y, run_gemm(A, W, torch.bfloat16).float().cpu().numpy())
+
+
+@pytest.mark.parametrize("fmt", ["mxfp4", "nvfp4"])
 def test_gemm_bf16_output_within_one_ulp(fmt):
     rng = np.random.default_rng(5)
     A, W = random_container(rng, 256, 1024, fmt), random_container(rng, 512, 1024, fmt)
