@@ -95,6 +95,14 @@ int mrfp4_act_quant(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ld
                     uint8_t* codes, uint8_t* sf, float* tensor_scale,
                     uint32_t* status, void* workspace, size_t workspace_bytes, void* stream);
 
+/* QuantResult metrics of an act-quant result (quantizers.py:218-231): accumulates into the
+ * caller-zeroed device acc[3] = {sum (y-q)^2, sum y^2, sum over groups of the squared relative
+ * error at the group's argmax |y|} (fp64, rotated domain); mse_rel = acc[0] / acc[1],
+ * mse_top_rel = acc[2] / (M * K / G).  Off the hot path. */
+int mrfp4_quant_metrics(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ldx, int fmt, int had_k,
+                        const uint8_t* codes, const uint8_t* sf, const float* tensor_scale, double* acc,
+                        void* stream);
+
 /* Row-major [rows, sf_cols] scale codes <-> swizzled layout (padding written as 0). */
 int mrfp4_sf_swizzle(const uint8_t* sf_rowmajor, uint8_t* sf_swizzled,
                      int64_t rows, int64_t sf_cols, void* stream);

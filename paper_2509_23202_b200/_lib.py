@@ -32,6 +32,7 @@ SIGNATURES = {
     "mrfp4_sf_bytes": (_sz, [_i64, _i64]),
     "mrfp4_act_quant_workspace": (_sz, [_i64, _i64, _int]),
     "mrfp4_act_quant": (_int, [_vp, _int, _i64, _i64, _i64, _int, _int, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "mrfp4_quant_metrics": (_int, [_vp, _int, _i64, _i64, _i64, _int, _int, _vp, _vp, _vp, _vp, _vp]),
     "mrfp4_sf_swizzle": (_int, [_vp, _vp, _i64, _i64, _vp]),
     "mrfp4_sf_unswizzle": (_int, [_vp, _vp, _i64, _i64, _vp]),
     "mrfp4_gemm_workspace": (_sz, [_i64, _i64, _i64, _int]),

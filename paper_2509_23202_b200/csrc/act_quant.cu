@@ -712,6 +712,80 @@ __global__ void __launch_bounds__(kThreads, 3) k_act_quant_nv(AQParams p) {
 }
 
 // ---------------------------------------------------------------------------
+// QuantResult metrics (quantizers.py:218-231): mse_rel = sum (y - q)^2 / sum y^2 and
+// mse_top_rel = mean over groups of ((y_top - q_top) / y_top)^2 at each group's argmax |y|
+// (first index on ties, like np.argmax), all in the rotated domain.  Sums in fp64 with
+// the rotated values y = RN64(S * c); accumulated per warp, then fp64 atomics into
+// acc[0..2] = {sum err^2, sum y^2, sum top ratio} (zeroed by the caller).
+// Off the hot path (quantized_linear never asks for it).
+// ---------------------------------------------------------------------------
+template <int IN, int FMT, int HK>
+__global__ void __launch_bounds__(kThreads) k_quant_metrics(AQParams p, double* acc) {
+  using C = InCfg<IN>;
+  constexpr int G = FMT == MRFP4_FMT_MXFP4 ? 32 : 16;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const float ts = *p.tensor_scale;
+  double e2 = 0.0, x2 = 0.0, top = 0.0;
+  const int64_t gw = (int64_t)blockIdx.x * kWarps + warp, tw = (int64_t)gridDim.x * kWarps;
+  for (int64_t item = gw; item < p.items; item += tw) {
+    const Cursor c = cursor_at(p, item, lane);
+    const int col0 = c.seg * kSeg;
+    const bool live = col0 < p.Ki && c.row < p.Mi;
+    const int nvalid = live ? min(kSeg, p.Ki - col0) : 0;
+    uint32_t w[kSeg * C::kEs / 4];
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(static_cast<const char*>(p.x) +
+                                                            ((uint64_t)c.row * p.ldx + (uint32_t)col0) * C::kEs);
+#pragma unroll
+    for (int j = 0; j < kSeg * C::kEs / 4; ++j) w[j] = (j * 4 < nvalid * C::kEs) ? src[j] : 0u;
+    u64 P[kPairs];
+#pragma unroll
+    for (int j = 0; j < kPairs; ++j) {
+      if constexpr (IN == MRFP4_DT_F32) {
+        P[j] = pk(__uint_as_float(w[2 * j]), __uint_as_float(w[2 * j + 1]));
+      } else if constexpr (IN == MRFP4_DT_BF16) {
+        P[j] = pk(__uint_as_float(w[j] << 16), __uint_as_float(w[j] & 0xFFFF0000u));
+      } else {
+        const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[j]));
+        P[j] = pk(f.x, f.y);
+      }
+    }
+    if constexpr (HK > 0) fwht<HK>(P, lane, p.pm);
+    if (!live) continue;
+    const uint8_t* cb = p.codes + (uint64_t)c.row * p.half_k + (uint32_t)(col0 >> 1);
+    for (int g0 = 0; g0 < nvalid; g0 += G) {
+      const int gcol = (col0 + g0) / G;
+      const uint32_t scode = p.sf[sf_off32(c.row, gcol, p.cb)];
+      const double dec = FMT == MRFP4_FMT_MXFP4 ? ldexp(1.0, (int)scode - 127) : (double)e4m3_value(scode);
+      const double eff = (double)ts * dec;
+      double best = -1.0, yt = 0.0, qt = 0.0;
+      for (int t = 0; t < G; ++t) {
+        const int e = g0 + t;
+        const float sv = (e & 1) ? hi_of(P[e >> 1]) : lo_of(P[e >> 1]);
+        const double y = (double)sv * p.c64;
+        const uint32_t code = (cb[e >> 1] >> (4 * (e & 1))) & 0xFu;
+        const float mag[8] = {0.f, 0.5f, 1.f, 1.5f, 2.f, 3.f, 4.f, 6.f};
+        const double q = eff * (double)((code & 8u) ? -mag[code & 7u] : mag[code & 7u]);
+        e2 += (y - q) * (y - q);
+        x2 += y * y;
+        if (fabs(y) > best) { best = fabs(y); yt = y; qt = q; }
+      }
+      if (yt != 0.0) top += (yt - qt) * (yt - qt) / (yt * yt);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    e2 += __shfl_xor_sync(0xffffffffu, e2, o);
+    x2 += __shfl_xor_sync(0xffffffffu, x2, o);
+    top += __shfl_xor_sync(0xffffffffu, top, o);
+  }
+  if (lane == 0) {
+    atomicAdd(acc, e2);
+    atomicAdd(acc + 1, x2);
+    atomicAdd(acc + 2, top);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
 int num_sms() {
@@ -772,9 +846,9 @@ int dispatch_fmt(const AQParams& p, int fmt, int hk, cudaStream_t s) {
 }  // namespace
 
 // Host launcher; arguments validated by the C-ABI layer (capi.cu).
-int launch_act_quant(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ldx, int fmt, int hk,
-                     uint8_t* codes, uint8_t* sf, float* tensor_scale, uint32_t* status,
-                     void* workspace, cudaStream_t s) {
+namespace {
+AQParams make_params(const void* x, int64_t M, int64_t K, int64_t ldx, int fmt, int hk, uint8_t* codes, uint8_t* sf,
+                     float* tensor_scale, uint32_t* status, void* workspace) {
   AQParams p;
   p.x = x;
   p.M = M;
@@ -809,6 +883,14 @@ int launch_act_quant(const void* x, int x_dtype, int64_t M, int64_t K, int64_t l
   p.c64 = hk ? 1.0 / sqrt((double)hk) : 1.0;
   p.kraw = (float)(p.c64 / 6.0);
   p.kmx = (float)(p.c64 / (double)1.33333337306976318359375f);
+  return p;
+}
+}  // namespace
+
+int launch_act_quant(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ldx, int fmt, int hk,
+                     uint8_t* codes, uint8_t* sf, float* tensor_scale, uint32_t* status,
+                     void* workspace, cudaStream_t s) {
+  const AQParams p = make_params(x, M, K, ldx, fmt, hk, codes, sf, tensor_scale, status, workspace);
   int rc;
   switch (x_dtype) {
     case MRFP4_DT_BF16: rc = dispatch_fmt<MRFP4_DT_BF16>(p, fmt, hk, s); break;
@@ -818,6 +900,29 @@ int launch_act_quant(const void* x, int x_dtype, int64_t M, int64_t K, int64_t l
   }
   if (rc != MRFP4_OK) return rc;
   return cudaPeekAtLastError() == cudaSuccess ? MRFP4_OK : MRFP4_ECUDA;
+}
+
+int launch_quant_metrics(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ldx, int fmt, int hk,
+                         const uint8_t* codes, const uint8_t* sf, const float* tensor_scale, double* acc,
+                         cudaStream_t s) {
+  const AQParams p = make_params(x, M, K, ldx, fmt, hk, const_cast<uint8_t*>(codes), const_cast<uint8_t*>(sf),
+                                 const_cast<float*>(tensor_scale), nullptr, nullptr);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(p.items, kWarps), 4 * num_sms()));
+  auto go = [&](auto kern) {
+    kern<<<grid, kThreads, 0, s>>>(p, acc);
+    return cudaPeekAtLastError() == cudaSuccess ? MRFP4_OK : MRFP4_ECUDA;
+  };
+#define MRFP4_MCASE(IN, FMT, HK) \
+  if (x_dtype == IN && fmt == FMT && hk == HK) return go(k_quant_metrics<IN, FMT, HK>);
+#define MRFP4_MFMT(IN, FMT) \
+  MRFP4_MCASE(IN, FMT, 0) MRFP4_MCASE(IN, FMT, 16) MRFP4_MCASE(IN, FMT, 32) MRFP4_MCASE(IN, FMT, 64) \
+  MRFP4_MCASE(IN, FMT, 128)
+  MRFP4_MFMT(MRFP4_DT_BF16, MRFP4_FMT_MXFP4) MRFP4_MFMT(MRFP4_DT_BF16, MRFP4_FMT_NVFP4)
+  MRFP4_MFMT(MRFP4_DT_F16, MRFP4_FMT_MXFP4) MRFP4_MFMT(MRFP4_DT_F16, MRFP4_FMT_NVFP4)
+  MRFP4_MFMT(MRFP4_DT_F32, MRFP4_FMT_MXFP4) MRFP4_MFMT(MRFP4_DT_F32, MRFP4_FMT_NVFP4)
+#undef MRFP4_MFMT
+#undef MRFP4_MCASE
+  return MRFP4_EUNSUPPORTED;
 }
 
 }  // namespace mrfp4

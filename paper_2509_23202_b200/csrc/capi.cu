@@ -16,6 +16,9 @@ int launch_gemm_fp4(const uint8_t* a, const uint8_t* a_sf, const float* a_ts, co
                     const float* b_ts, void* d, int d_dtype, int64_t M, int64_t N, int64_t K, int64_t ldd, int fmt,
                     void* ws, size_t ws_bytes, cudaStream_t s);
 size_t gemm_workspace_bytes(int64_t M, int64_t N, int64_t K);
+int launch_quant_metrics(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ldx, int fmt, int hk,
+                         const uint8_t* codes, const uint8_t* sf, const float* tensor_scale, double* acc,
+                         cudaStream_t s);
 int launch_sf_swizzle(const uint8_t* src, uint8_t* dst, int64_t rows, int64_t cols, cudaStream_t s);
 int launch_sf_unswizzle(const uint8_t* src, uint8_t* dst, int64_t rows, int64_t cols, cudaStream_t s);
 int launch_dequantize(const uint8_t* codes, const uint8_t* sf, const float* ts, int64_t rows, int64_t cols, int fmt,
@@ -100,6 +103,21 @@ int mrfp4_act_quant(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ld
   const int rc = mrfp4::launch_act_quant(x, x_dtype, M, K, ldx, fmt, had_k, codes, sf, tensor_scale, status,
                                          workspace, static_cast<cudaStream_t>(stream));
   return cuda_status(rc, "mrfp4_act_quant");
+}
+
+int mrfp4_quant_metrics(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ldx, int fmt, int had_k,
+                        const uint8_t* codes, const uint8_t* sf, const float* tensor_scale, double* acc,
+                        void* stream) {
+  const int G = mrfp4_group_size(fmt);
+  if (G == 0) return fail(MRFP4_EUNSUPPORTED, "unknown format %d", fmt);
+  const int es = elt_size(x_dtype);
+  if (es == 0) return fail(MRFP4_EUNSUPPORTED, "unsupported input dtype %d", x_dtype);
+  if (M < 1 || K < 1 || K % G || (had_k && K % had_k) || ldx < K) return fail(MRFP4_EINVAL, "bad dimensions");
+  if (!x || !codes || !sf || !tensor_scale || !acc) return fail(MRFP4_EINVAL, "null buffer");
+  if (((uint64_t)ldx * es) % 16 || !aligned(x, 16)) return fail(MRFP4_EUNSUPPORTED, "input rows must be 16-byte aligned");
+  return cuda_status(mrfp4::launch_quant_metrics(x, x_dtype, M, K, ldx, fmt, had_k, codes, sf, tensor_scale, acc,
+                                                 static_cast<cudaStream_t>(stream)),
+                     "mrfp4_quant_metrics");
 }
 
 int mrfp4_sf_swizzle(const uint8_t* src, uint8_t* dst, int64_t rows, int64_t cols, void* stream) {

@@ -76,6 +76,8 @@ class GpuQuantResult:
     sf: torch.Tensor               # uint8, swizzled 128x4-atom layout
     tensor_scale_dev: torch.Tensor  # float32 [1]
     scratch: torch.Tensor          # int32 [8]: [0] status bits, [4:] workspace
+    source: torch.Tensor | None = None   # the input X (for the lazily computed metrics)
+    _metrics: tuple | None = None
 
     @property
     def spec(self):
@@ -120,6 +122,31 @@ class GpuQuantResult:
     def tensor(self) -> MfpTensor:
         return self.to_mfp()
 
+    def metrics(self) -> tuple[float, float]:
+        """(mse_rel, mse_top_rel) of the reference's QuantResult (quantizers.py:218-231),
+        computed on the device in fp64 in the rotated domain (first call synchronizes)."""
+        if self._metrics is None:
+            if self.source is None:
+                raise DataError("metrics need the quantized input (result built without a source)")
+            X = self.source
+            acc = torch.zeros(3, dtype=torch.float64, device=self.codes.device)
+            _lib.check(_lib.lib().mrfp4_quant_metrics(
+                _lib.ptr(X), _DT[X.dtype], self.rows, self.cols, X.stride(0), self.fmt, self.had_k,
+                _lib.ptr(self.codes), _lib.ptr(self.sf), _lib.ptr(self.tensor_scale_dev), _lib.ptr(acc),
+                _lib.stream_ptr(torch, X.device)))
+            e2, x2, top = acc.tolist()
+            n_groups = self.rows * (self.cols // self.group_size)
+            self._metrics = (e2 / x2 if x2 > 0 else 0.0, top / n_groups)
+        return self._metrics
+
+    @property
+    def mse_rel(self) -> float:
+        return self.metrics()[0]
+
+    @property
+    def mse_top_rel(self) -> float:
+        return self.metrics()[1]
+
 
 def act_quant_into(X: torch.Tensor, fmt: int, had_k: int, codes: torch.Tensor, sf: torch.Tensor,
                    ts: torch.Tensor, scratch: torch.Tensor) -> None:
@@ -163,6 +190,7 @@ def quantize_rtn(X, spec, policy=None, transform=None, *, check: bool = True) ->
         raise DataError(f"columns ({K}) not divisible by transform block ({had_k})")
     res = alloc_result(M, K, fmt, had_k, X.device)
     act_quant_into(X, fmt, had_k, res.codes, res.sf, res.tensor_scale_dev, res.scratch)
+    res.source = X
     if check:
         res.check()
     return res

@@ -211,3 +211,30 @@ def test_nonfinite_anywhere_in_group_raises(fmt, k, bad):
         X[r, c] = bad
         with pytest.raises(P.DataError):
             P.quantize_rtn(_gpu(X), SPEC[fmt], transform=_tr(k))
+
+
+@pytest.mark.parametrize("fmt,k", [("mxfp4", 32), ("nvfp4", 16), ("nvfp4", 128), ("mxfp4", 0)])
+def test_metrics_match_reference(fmt, k):
+    """QuantResult.mse_rel / mse_top_rel (quantizers.py:218-231), fp64 on the device.
+    Floating-point statistics: tolerance 1e-6 relative (the fp32 FWHT inputs differ from
+    the reference's fp64 BLAS rotation by ~1e-8 for k = 128)."""
+    rng = np.random.default_rng(17)
+    X = O.bf16_round(rng.standard_normal((96, 1024)) * np.exp2(rng.integers(-3, 4, (96, 1))))
+    ora = O.quantize_rtn(X, fmt, hadamard=k or None)
+    gpu = P.quantize_rtn(_gpu(X), SPEC[fmt], transform=_tr(k))
+    assert gpu.mse_rel == pytest.approx(ora.mse_rel, rel=1e-6)
+    assert gpu.mse_top_rel == pytest.approx(ora.mse_top_rel, rel=1e-6)
+
+
+def test_metrics_against_golden(golden):
+    """Same, against metrics the real reference produced for the golden fixtures."""
+    n = 0
+    for key in _keys(golden, "rand_"):
+        if key + "_mse" not in golden.files or key + "_raises" in golden.files:
+            continue
+        fmt, k = key.split("_")[-2], int(key.split("_")[-1][1:])
+        gpu = P.quantize_rtn(_gpu(golden[key + "_x"]), SPEC[fmt], transform=_tr(k))
+        assert gpu.mse_rel == pytest.approx(float(golden[key + "_mse"]), rel=1e-6), key
+        assert gpu.mse_top_rel == pytest.approx(float(golden[key + "_msetop"]), rel=1e-6), key
+        n += 1
+    assert n > 0
