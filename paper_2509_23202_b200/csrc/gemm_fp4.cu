@@ -71,6 +71,7 @@ struct GemmArgs {
   int64_t b_row_blocks;   // ceil(N / 128)
   int num_m_blk, num_n_blk, num_kb;
   int tail_mmas;  // MMAs in the last k-block (0 = full)
+  int preissue;   // 2-CTA kernel: issue the first weight stages before the PDL wait
   int splits;     // 1-CTA kernel: K splits per output tile (> 1: fp32 partials to `ws`)
   int kb_per;     // k-blocks per split
   float* ws;      // [splits][M][N] fp32 partial sums (splits > 1)
@@ -556,44 +557,79 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(448, 1)
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------------------- producer
-      pdl_wait();  // A, its scale factors and tensor scale come from the act-quant kernel
+      // The weight (B, SFB) does not depend on the act-quant kernel: the first stages'
+      // weight loads are issued BEFORE the PDL wait, so their latency hides behind K1's
+      // tail; A / SFA follow once K1 has completed.
       Ring ab, sf;
       WorkIter it(g, cluster, nclusters);
       Work w;
-      while (it.next(g, w)) {
-        const int m_blk = w.tile % num_m_blk, n_blk = w.tile / num_m_blk;
-        for (int kb = w.kb0; kb < w.kb1; ++kb) {
-          sm100::mbar_wait(&sf_empty[sf.idx], sf.ph ^ 1);
-          {
-            // Scale factors: contiguous 512-B atoms per 128-row block -> 1-D bulk copies
-            // (K tail: copy only the atoms that exist; the rest of the slot is never read
-            // by an issued MMA).  Row blocks past the end of A / B are skipped.
-            const int64_t katom = (int64_t)kb * C::kAtoms;
-            const uint32_t nat = (uint32_t)imin64(C::kAtoms, sf_col_blocks - katom) * 512u;
-            const int64_t ra = (int64_t)m_blk * 2 + rank;
-            const int64_t rb0 = (int64_t)n_blk * 2;
-            const uint32_t bytes = (ra < a_row_blocks ? nat : 0u) + (rb0 < b_row_blocks ? nat : 0u) +
-                                   (rb0 + 1 < b_row_blocks ? nat : 0u);
-            sm100::mbar_arrive_expect_tx(&sf_full[sf.idx], bytes);
-            if (ra < a_row_blocks)
-              sm100::bulk_load(smem + C::kOffSfa + sf.idx * C::kSfaBytes, g.a_sf + (ra * sf_col_blocks + katom) * 512,
-                               nat, &sf_full[sf.idx]);
+      auto sf_bytes = [&](int kb, int m_blk, int n_blk, uint32_t& nat, bool& has_a, int& nb) {
+        const int64_t katom = (int64_t)kb * C::kAtoms;
+        nat = (uint32_t)imin64(C::kAtoms, sf_col_blocks - katom) * 512u;
+        has_a = (int64_t)m_blk * 2 + rank < a_row_blocks;
+        nb = ((int64_t)n_blk * 2 < b_row_blocks) + ((int64_t)n_blk * 2 + 1 < b_row_blocks);
+      };
+      auto load_b = [&](int kb, int n_blk, int abi, int sfi) {  // SFB + B of one stage
+        const int64_t katom = (int64_t)kb * C::kAtoms;
+        const uint32_t nat = (uint32_t)imin64(C::kAtoms, sf_col_blocks - katom) * 512u;
+        const int64_t rb0 = (int64_t)n_blk * 2;
 #pragma unroll
-            for (int j = 0; j < 2; ++j)
-              if (rb0 + j < b_row_blocks)
-                sm100::bulk_load(smem + C::kOffSfb + sf.idx * C::kSfbBytes + j * C::kSfaBytes,
-                                 g.b_sf + ((rb0 + j) * sf_col_blocks + katom) * 512, nat, &sf_full[sf.idx]);
-          }
-          sf.next<C::kSfSlots>();
-          sm100::mbar_wait(&empty[ab.idx], ab.ph ^ 1);
-          if (leader) sm100::mbar_arrive_expect_tx(&full[ab.idx], 2u * (C::kABytes + C::kBBytes));
-          const uint32_t lb = sm100::leader_bar(&full[ab.idx]);
-          tma_load_3d_2sm(smem + C::kOffA + ab.idx * C::kABytes, &tmA, lb, m_blk * 256 + (int)rank * 128,
-                          kb * C::kSlices);
-          tma_load_3d_2sm(smem + C::kOffB + ab.idx * C::kBBytes, &tmB, lb, n_blk * 256 + (int)rank * 128,
-                          kb * C::kSlices);
-          ab.next<C::kStages>();
+        for (int j = 0; j < 2; ++j)
+          if (rb0 + j < b_row_blocks)
+            sm100::bulk_load(smem + C::kOffSfb + sfi * C::kSfbBytes + j * C::kSfaBytes,
+                             g.b_sf + ((rb0 + j) * sf_col_blocks + katom) * 512, nat, &sf_full[sfi]);
+        tma_load_3d_2sm(smem + C::kOffB + abi * C::kBBytes, &tmB, sm100::leader_bar(&full[abi]),
+                        n_blk * 256 + (int)rank * 128, kb * C::kSlices);
+      };
+      auto load_a = [&](int kb, int m_blk, int abi, int sfi) {  // SFA + A of one stage
+        const int64_t katom = (int64_t)kb * C::kAtoms;
+        const uint32_t nat = (uint32_t)imin64(C::kAtoms, sf_col_blocks - katom) * 512u;
+        const int64_t ra = (int64_t)m_blk * 2 + rank;
+        if (ra < a_row_blocks)
+          sm100::bulk_load(smem + C::kOffSfa + sfi * C::kSfaBytes, g.a_sf + (ra * sf_col_blocks + katom) * 512, nat,
+                           &sf_full[sfi]);
+        tma_load_3d_2sm(smem + C::kOffA + abi * C::kABytes, &tmA, sm100::leader_bar(&full[abi]),
+                        m_blk * 256 + (int)rank * 128, kb * C::kSlices);
+      };
+      auto arm = [&](int kb, int m_blk, int n_blk, int abi, int sfi) {  // expect all bytes of a stage
+        uint32_t nat;
+        bool has_a;
+        int nb;
+        sf_bytes(kb, m_blk, n_blk, nat, has_a, nb);
+        sm100::mbar_arrive_expect_tx(&sf_full[sfi], (has_a ? nat : 0u) + nat * (uint32_t)nb);
+        if (leader) sm100::mbar_arrive_expect_tx(&full[abi], 2u * (C::kABytes + C::kBBytes));
+      };
+      int pre = 0;  // stages of the first item whose weight half was issued before the PDL wait
+      if (it.next(g, w)) {
+        const int m_blk = w.tile % num_m_blk, n_blk = w.tile / num_m_blk;
+        pre = g.preissue ? min(min(C::kStages, C::kSfSlots), w.kb1 - w.kb0) : 0;
+        for (int s2 = 0; s2 < pre; ++s2) {  // fresh barriers: no empty waits needed
+          arm(w.kb0 + s2, m_blk, n_blk, s2, s2);
+          load_b(w.kb0 + s2, n_blk, s2, s2);
         }
+        pdl_wait();  // A, its scale factors and tensor scale come from the act-quant kernel
+        for (int s2 = 0; s2 < pre; ++s2) load_a(w.kb0 + s2, m_blk, s2, s2);
+        for (int s2 = 0; s2 < pre; ++s2) {
+          ab.next<C::kStages>();
+          sf.next<C::kSfSlots>();
+        }
+        bool more = true;
+        while (more) {
+          const int mb = w.tile % num_m_blk, nb = w.tile / num_m_blk;
+          for (int kb = w.kb0 + pre; kb < w.kb1; ++kb) {
+            sm100::mbar_wait(&sf_empty[sf.idx], sf.ph ^ 1);
+            sm100::mbar_wait(&empty[ab.idx], ab.ph ^ 1);
+            arm(kb, mb, nb, ab.idx, sf.idx);
+            load_a(kb, mb, ab.idx, sf.idx);
+            load_b(kb, nb, ab.idx, sf.idx);
+            ab.next<C::kStages>();
+            sf.next<C::kSfSlots>();
+          }
+          pre = 0;
+          more = it.next(g, w);
+        }
+      } else {
+        pdl_wait();
       }
     }
   } else if (warp == 1) {
@@ -923,12 +959,14 @@ int g_debug_mode = 0;
 unsigned long long* g_debug_buf = nullptr;
 int g_force_grid = 0;
 int g_force_kernel = 0;  // 0 auto, 1 = 1-CTA kernel, 2 = 2-CTA kernel
+int g_preissue = 1;
 
 int launch_gemm_fp4(const uint8_t* a, const uint8_t* a_sf, const float* a_ts, const uint8_t* b, const uint8_t* b_sf,
                     const float* b_ts, void* d, int d_dtype, int64_t M, int64_t N, int64_t K, int64_t ldd, int fmt,
                     void* ws, size_t ws_bytes, cudaStream_t s) {
   GemmArgs g{};
   g.b = b;
+  g.preissue = g_preissue;
   g.ws = static_cast<float*>(ws);
   g.ws_bytes = ws_bytes;
   g.debug = g_debug_mode;
@@ -963,6 +1001,8 @@ int launch_gemm_fp4(const uint8_t* a, const uint8_t* a_sf, const float* a_ts, co
 extern "C" void mrfp4_debug_gemm_grid(int g) { mrfp4::g_force_grid = g; }
 
 extern "C" void mrfp4_debug_gemm_timestamps(unsigned long long* dev_buf) { mrfp4::g_debug_buf = dev_buf; }
+
+extern "C" void mrfp4_debug_gemm_preissue(int on) { mrfp4::g_preissue = on; }
 
 extern "C" int mrfp4_debug_gemm_kernel(int which) {
   const int old = mrfp4::g_force_kernel;
