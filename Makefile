@@ -14,7 +14,7 @@ all: $(LIB)
 
 build/obj/%.o: $(PKG)/csrc/%.cu $(HDR)
 	@mkdir -p build/obj
-	$(NVCC) $(NVFLAGS) -c $< -o $@
+	$(NVCC) $(NVFLAGS) $(EXTRA) -c $< -o $@
 
 $(LIB): $(OBJ)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJ) -Xlinker --no-undefined -lcuda 2>/dev/null || \

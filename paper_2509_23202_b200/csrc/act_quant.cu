@@ -33,7 +33,10 @@
 // hardware E2M1 conversion, from u * (1 +- 2^-18) (the fp32 u ~ y / eff is within
 // 2^-21 of the exact quotient), and any element whose two roundings disagree is
 // re-decided from u = RN64(y / eff) exactly as numpy does (quantizers.py:213).
+#include <cudaTypedefs.h>
+
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -41,20 +44,26 @@
 
 namespace mrfp4 {
 
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder();  // gemm_fp4.cu
+
 namespace {
 
 constexpr int kSeg = 32;       // elements per lane segment
 constexpr int kPairs = kSeg / 2;
-constexpr int kWarps = 8;      // warps per CTA
-constexpr int kThreads = kWarps * 32;
-constexpr int kStages = 3;     // cp.async ring depth per lane
+constexpr int kMetricWarps = 8;
+#ifndef MRFP4_K1_STAGES
+#define MRFP4_K1_STAGES 3
+#endif
+constexpr int kMaxStages = 3;
 
 template <int IN>
 struct InCfg {
   static constexpr int kEs = IN == MRFP4_DT_F32 ? 4 : 2;
   static constexpr int kChunks = kSeg * kEs / 16;          // 16-B chunks per segment: 4 or 8
   static constexpr int kLaneBytes = kSeg * kEs;
-  static constexpr int kSmem = kWarps * kStages * 32 * kLaneBytes;
+  // ring depth per warp (f32 rows are twice as long: 2 stages fit the 227 KB of SMEM)
+  static constexpr int kStages = kEs == 4 ? 2 : MRFP4_K1_STAGES;
+  static constexpr int smem(int warps) { return warps * kStages * 32 * kLaneBytes + 1024; }  // + 1 KB alignment
 };
 
 struct AQParams {
@@ -69,6 +78,7 @@ struct AQParams {
   int64_t sf_col_blocks;   // ceil(sf_cols / 4)
   int64_t rows_pad;        // ceil(M / 128) * 128
   int64_t items;           // warp items
+  uint32_t div_m;          // ceil(2^32 / div_d): FlatWalk divides by nseg, GenWalk by nchunk
   int nchunk;              // column chunks of L segments per row group
   int seg_span;            // nchunk * L
   int lane_bits;           // log2(L)
@@ -79,6 +89,11 @@ struct AQParams {
   int Mi, Ki;              // M, K as 32-bit (the C-ABI checks they fit)
   uint32_t half_k;         // K / 2: bytes per code row
   uint32_t cb;             // sf_col_blocks as 32-bit
+  unsigned long long* trace;  // perf experiments: per-warp globaltimer stamps (null in production)
+  uint64_t x_bytes;         // M * K * element size
+  int marks;                // NVFP4 ring-resident re-encode: -1 auto, 0 off, 1 on
+  int nseg;                // flat walk: segments per row (K / 32)
+  uint32_t total_segs;     // flat walk: M * K / 32
 };
 
 // ---------------------------------------------------------------------------
@@ -151,44 +166,102 @@ __device__ __forceinline__ uint32_t swz(int j, int lane) {
 
 // A lane's position: row and 32-element column segment of the current warp item.
 // Items are row-group-major (item = rg * nchunk + cc); a warp walks a contiguous range.
-struct Cursor {
-  int row;
-  int seg;
+// Two walkers share one interface (at / step / issue / live / full / row / seg / cdst):
+//   GenWalk  -- any K and row stride: L = 2^lane_bits lanes per row chunk, ragged tails
+//               zero-filled.
+//   FlatWalk -- contiguous rows (ldx == K), K % 32 == 0, K >= 1024: lane segment
+//               s = 32 * item + lane of the flattened matrix, so a segment is 64 contiguous
+//               bytes, never straddles a row, and the row / column cursor is one compare per
+//               step.  Lane groups of 2 / 4 (H64 / H128 shuffles) stay inside one Hadamard
+//               block because K % k == 0.
+// n / d for n < 2^31 with m = ceil(2^32 / d) (m = 0 encodes d = 1): the estimate is exact or
+// one too large.
+__device__ __forceinline__ uint32_t fast_div(uint32_t n, uint32_t d, uint32_t m) {
+  uint32_t q = m ? __umulhi(n, m) : n;
+  if ((int)(n - q * d) < 0) --q;
+  return q;
+}
+
+struct GenWalk {
+  static constexpr bool kTma = false;
+  int row_, seg_;
+  __device__ __forceinline__ void at(const AQParams& p, int item, int lane) {
+    const int rg = (int)fast_div((uint32_t)item, (uint32_t)p.nchunk, p.div_m);
+    const int cc = item - rg * p.nchunk;
+    row_ = (int)(rg * (32 >> p.lane_bits)) + (lane >> p.lane_bits);
+    seg_ = (cc << p.lane_bits) + (lane & ((1 << p.lane_bits) - 1));
+  }
+  template <int DIR>
+  __device__ __forceinline__ void step(const AQParams& p) {
+    if constexpr (DIR > 0) {
+      seg_ += 1 << p.lane_bits;
+      if (seg_ >= p.seg_span) { seg_ -= p.seg_span; row_ += 32 >> p.lane_bits; }
+    } else {
+      seg_ -= 1 << p.lane_bits;
+      if (seg_ < 0) { seg_ += p.seg_span; row_ -= 32 >> p.lane_bits; }
+    }
+  }
+  template <int IN>
+  __device__ __forceinline__ void issue(const AQParams& p, uint32_t sbase, int lane) const;
+  __device__ __forceinline__ bool live(const AQParams& p) const { return seg_ * kSeg < p.Ki && row_ < p.Mi; }
+  __device__ __forceinline__ bool full(const AQParams& p) const { return seg_ * kSeg + kSeg <= p.Ki; }
+  __device__ __forceinline__ int row() const { return row_; }
+  __device__ __forceinline__ int seg() const { return seg_; }
+  __device__ __forceinline__ uint8_t* cdst(const AQParams& p) const {
+    return p.codes + (uint64_t)row_ * p.half_k + (uint32_t)(seg_ * (kSeg / 2));
+  }
 };
 
-__device__ __forceinline__ Cursor cursor_at(const AQParams& p, int64_t item, int lane) {
-  const int64_t rg = item / p.nchunk;
-  const int cc = (int)(item - rg * p.nchunk);
-  Cursor c;
-  c.row = (int)(rg * (32 >> p.lane_bits)) + (lane >> p.lane_bits);
-  c.seg = (cc << p.lane_bits) + (lane & ((1 << p.lane_bits) - 1));
-  return c;
-}
-
-template <int DIR>
-__device__ __forceinline__ void cursor_step(const AQParams& p, Cursor& c) {
-  if constexpr (DIR > 0) {
-    c.seg += 1 << p.lane_bits;
-    if (c.seg >= p.seg_span) { c.seg -= p.seg_span; c.row += 32 >> p.lane_bits; }
-  } else {
-    c.seg -= 1 << p.lane_bits;
-    if (c.seg < 0) { c.seg += p.seg_span; c.row -= 32 >> p.lane_bits; }
+struct FlatWalk {
+  static constexpr bool kTma = true;
+  uint32_t s_;
+  int row_, seg_;
+  __device__ __forceinline__ void at(const AQParams& p, int item, int lane) {
+    s_ = (uint32_t)item * 32u + (uint32_t)lane;
+    row_ = (int)fast_div(s_, (uint32_t)p.nseg, p.div_m);
+    seg_ = (int)(s_ - (uint32_t)row_ * (uint32_t)p.nseg);
   }
-}
+  template <int DIR>
+  __device__ __forceinline__ void step(const AQParams& p) {
+    if constexpr (DIR > 0) {
+      s_ += 32u;
+      seg_ += 32;
+      if (seg_ >= p.nseg) { seg_ -= p.nseg; ++row_; }
+    } else {
+      s_ -= 32u;
+      seg_ -= 32;
+      if (seg_ < 0) { seg_ += p.nseg; --row_; }
+    }
+  }
+  template <int IN>
+  __device__ __forceinline__ void issue(const AQParams& p, uint32_t sbase, int lane) const {
+    using C = InCfg<IN>;
+    if (s_ < p.total_segs) {
+      const char* src = static_cast<const char*>(p.x) + (uint64_t)s_ * C::kLaneBytes;
+#pragma unroll
+      for (int j = 0; j < C::kChunks; ++j) cp_async16(sbase + swz<IN>(j, lane) * 16, src + j * 16, 16u);
+    }
+  }
+  __device__ __forceinline__ bool live(const AQParams& p) const { return s_ < p.total_segs; }
+  __device__ __forceinline__ bool full(const AQParams&) const { return true; }
+  __device__ __forceinline__ int row() const { return row_; }
+  __device__ __forceinline__ int seg() const { return seg_; }
+  __device__ __forceinline__ uint8_t* cdst(const AQParams& p) const { return p.codes + (uint64_t)s_ * (kSeg / 2); }
+};
 
 template <int IN>
-__device__ __forceinline__ void issue_seg(const AQParams& p, const Cursor& c, uint32_t sbase, int lane) {
+__device__ __forceinline__ void GenWalk::issue(const AQParams& p, uint32_t sbase, int lane) const {
   using C = InCfg<IN>;
-  const int col0 = c.seg * kSeg;
+  const int col0 = seg_ * kSeg;
   const char* x = static_cast<const char*>(p.x);
-  if (c.row < p.Mi && col0 + kSeg <= p.Ki) {  // interior segment
-    const char* src = x + ((uint64_t)c.row * (uint64_t)p.ldx + (uint32_t)col0) * C::kEs;
+  if (row_ < p.Mi && col0 + kSeg <= p.Ki) {  // interior segment
+    const char* src = x + ((uint64_t)row_ * (uint64_t)p.ldx + (uint32_t)col0) * C::kEs;
 #pragma unroll
     for (int j = 0; j < C::kChunks; ++j) cp_async16(sbase + swz<IN>(j, lane) * 16, src + j * 16, 16u);
     return;
   }
-  const int nb = (col0 < p.Ki && c.row < p.Mi) ? (p.Ki - col0) * C::kEs : 0;  // < kSeg * kEs here
-  const char* src = nb ? x + ((uint64_t)c.row * (uint64_t)p.ldx + (uint32_t)col0) * C::kEs : x;
+  const int nb = (col0 < p.Ki && row_ < p.Mi) ? (p.Ki - col0) * C::kEs : 0;  // < kSeg * kEs here
+  const char* src = nb ? x + ((uint64_t)row_ * (uint64_t)p.ldx + (uint32_t)col0) * C::kEs : x;
 #pragma unroll
   for (int j = 0; j < C::kChunks; ++j) {
     const int rem = nb - j * 16;
@@ -453,54 +526,168 @@ __device__ __forceinline__ void quantize_seg(const u64 (&P)[kPairs], const Group
 // ---------------------------------------------------------------------------
 // kernels
 // ---------------------------------------------------------------------------
-// Persistent per-lane pipeline over this warp's contiguous item range: issue segment
-// i+2 while segment i is processed.  DIR = -1 walks the range backwards (NVFP4 phase
-// 2 re-reads X; start with what phase 1 left most recently in L2).
-// PDL: EARLY = true issues the first loads before waiting for the predecessor grid
-// (only when X is not produced by it, i.e. NVFP4 phase 2 after phase 1); `ready` runs
-// once after the wait, before the first segment is processed.
-template <int IN, int DIR, bool EARLY, typename R, typename F>
-__device__ __forceinline__ void for_each_seg(const AQParams& p, R&& ready, F&& body) {
-  using C = InCfg<IN>;
-  extern __shared__ __align__(128) uint8_t smem_raw[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t gw = (int64_t)blockIdx.x * kWarps + warp, tw = (int64_t)gridDim.x * kWarps;
-  const int64_t i0 = gw * p.items / tw, i1 = (gw + 1) * p.items / tw;
-  const int n = (int)(i1 - i0);
-  if constexpr (!EARLY) pdl_wait();
-  if (n <= 0) {
-    if constexpr (EARLY) pdl_wait();
-    ready();
-    return;
+// Work split: CTA b (one per SM) owns the contiguous items [c0, c1); its warps claim them
+// one at a time from a shared-memory counter.  DRAM service is far from uniform across the
+// warps of a grid (per-warp first-load latency ranges 1.5-11 us at 2048x14336), so a static
+// per-warp split ends when the unluckiest warp does; a per-SM queue lets the SM's other warps
+// absorb it (scripts/k1_trace.py).  A claim is made one item ahead, hiding its latency.
+struct CtaRange {
+  int c0, cnt;
+  __device__ __forceinline__ void init(const AQParams& p) {
+    c0 = (int)((int64_t)blockIdx.x * p.items / gridDim.x);
+    cnt = (int)((int64_t)(blockIdx.x + 1) * p.items / gridDim.x) - c0;
   }
-  const uint32_t base =
-      (uint32_t)__cvta_generic_to_shared(smem_raw) + (uint32_t)((warp * kStages * 32 + lane) * C::kLaneBytes);
-  constexpr uint32_t kStride = 32 * C::kLaneBytes;
-  Cursor ci = cursor_at(p, DIR > 0 ? i0 : i1 - 1, lane), cp = ci;
+};
+
+struct Claims {
+  uint32_t* ctr;   // shared-memory counter
+  int cnt;
+  uint32_t pend;   // lane 0: claimed index (claimed one item ahead)
+  bool live;
+  __device__ __forceinline__ void init(uint32_t* c, int n, int lane) {
+    ctr = c;
+    cnt = n;
+    live = true;
+    if (lane == 0) pend = atomicAdd(ctr, 1u);
+  }
+  // Next claimed index in [0, cnt), or -1 once the range is exhausted (then forever -1).
+  __device__ __forceinline__ int next(int lane) {
+    if (!live) return -1;
+    const int c = (int)__shfl_sync(0xffffffffu, pend, 0);
+    if (c >= cnt) { live = false; return -1; }
+    if (lane == 0) pend = atomicAdd(ctr, 1u);
+    return c;
+  }
+};
+
+// Per-warp ring of kStages item slots (32 lane segments each) in shared memory.
+//   GenWalk (cp.async): every lane copies its own segment in 16-B chunks, XOR-swizzled by
+//     lane so the 16-B shared loads are bank-conflict free.
+//   FlatWalk (TMA): lane 0 issues one 2-D tensor copy of the item's 32 contiguous segments;
+//     the 64-B (bf16 / f16) or 128-B (f32) TMA swizzle produces exactly the same layout, and
+//     completion is tracked by one mbarrier per slot.  One request per 2-4 KB instead of 128.
+template <int IN, typename W>
+struct Loader {
+  using C = InCfg<IN>;
+  static constexpr int kStages = C::kStages;
+  static constexpr uint32_t kStride = 32 * C::kLaneBytes;
+  uint32_t wbase, lbase, bars, ph;
+  int lane;
+  __device__ __forceinline__ void init(uint32_t ring, uint32_t bar_addr, int lane_) {
+    lane = lane_;
+    wbase = ring;
+    lbase = ring + (uint32_t)lane_ * C::kLaneBytes;
+    bars = bar_addr;
+    ph = 0;
+    if constexpr (W::kTma) {
+      if (lane == 0) {
+#pragma unroll
+        for (int s = 0; s < kStages; ++s)
+          asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bars + 8 * s));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      }
+      __syncwarp();
+    }
+  }
+  __device__ __forceinline__ uint32_t slot(int s) const { return lbase + (uint32_t)s * kStride; }
+  __device__ __forceinline__ void issue(const AQParams& p, const CUtensorMap* tm, int item, int s) {
+    if constexpr (W::kTma) {
+      if (lane == 0) {
+        const uint32_t bar = bars + 8 * s;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(kStride) : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%3, %4}], [%2];" ::"r"(wbase + (uint32_t)s * kStride),
+            "l"(reinterpret_cast<uint64_t>(tm)), "r"(bar), "r"(0), "r"(item * 32)
+            : "memory");
+      }
+    } else {
+      W c;
+      c.at(p, item, lane);
+      c.template issue<IN>(p, slot(s), lane);
+    }
+  }
+  __device__ __forceinline__ void commit() {
+    if constexpr (!W::kTma) cp_commit();
+  }
+  // Data of the oldest outstanding slot `s` has landed (cp.async: all but kStages-1 groups).
+  __device__ __forceinline__ void wait(int s) {
+    if constexpr (W::kTma) {
+      const uint32_t par = (ph >> s) & 1u;
+      asm volatile(
+          "{\n\t.reg .pred P1;\n"
+          "WAIT_%=:\n\t"
+          "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+          "@!P1 bra WAIT_%=;\n\t}" ::"r"(bars + 8 * s),
+          "r"(par)
+          : "memory");
+      ph ^= 1u << s;
+    } else {
+      cp_wait<kStages - 1>();
+    }
+  }
+  __device__ __forceinline__ void wait_all() {
+    if constexpr (!W::kTma) cp_wait<0>();
+  }
+  // Before a slot this warp has read is refilled by the async proxy.
+  __device__ __forceinline__ void release() {
+    if constexpr (W::kTma) {
+      __syncwarp();
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+  }
+};
+
+// The warp's ring: kStages slots in dynamic shared memory (1 KB aligned for the TMA swizzle),
+// mbarriers in static shared memory.
+template <int NW, int IN, typename W>
+__device__ __forceinline__ void init_loader(Loader<IN, W>& L, int warp, int lane) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  constexpr int kStages = InCfg<IN>::kStages;
+  __shared__ __align__(8) uint64_t bars[NW * kMaxStages];
+  const uint32_t base = ((uint32_t)__cvta_generic_to_shared(smem_raw) + 1023u) & ~1023u;
+  L.init(base + (uint32_t)warp * kStages * Loader<IN, W>::kStride,
+         (uint32_t)__cvta_generic_to_shared(&bars[warp * kMaxStages]), lane);
+}
+
+// Per-warp pipeline over the items `next()` yields (-1 = done): issue item j+kStages-1 while
+// item j is processed; item j of the walk sits in ring slot j % kStages.  `resident[s]`
+// (warp-private shared memory) receives the last item processed from slot s (-1: none).
+template <int IN, typename W, typename N, typename F>
+__device__ __forceinline__ int run_pipeline(const AQParams& p, const CUtensorMap* tm, Loader<IN, W>& L, N&& next,
+                                            int* resident, F&& body) {
+  constexpr int kStages = InCfg<IN>::kStages;
+  const int lane = threadIdx.x & 31;
+  int it[kStages];
+  L.release();
 #pragma unroll
   for (int s = 0; s < kStages - 1; ++s) {
-    if (s < n) {
-      issue_seg<IN>(p, ci, base + s * kStride, lane);
-      cursor_step<DIR>(p, ci);
-    }
-    cp_commit();
+    it[s] = next();
+    if (it[s] >= 0) L.issue(p, tm, it[s], s);
+    L.commit();
   }
-  if constexpr (EARLY) pdl_wait();
-  ready();
-  int rd = 0, wr = kStages - 1;
-  for (int k = 0; k < n; ++k) {
-    if (k + kStages - 1 < n) {
-      issue_seg<IN>(p, ci, base + wr * kStride, lane);
-      cursor_step<DIR>(p, ci);
+  int rd = 0, wr = kStages - 1, n = 0;
+  while (true) {
+    it[kStages - 1] = next();
+    if (it[kStages - 1] >= 0) {
+      L.release();
+      L.issue(p, tm, it[kStages - 1], wr);
     }
-    cp_commit();
-    cp_wait<kStages - 1>();
-    body(cp, base + rd * kStride);
-    cursor_step<DIR>(p, cp);
+    L.commit();
+    if (it[0] < 0) break;
+    L.wait(rd);
+    W c;
+    c.at(p, it[0], lane);
+    body(c, L.slot(rd));
+    if (resident && lane == 0) resident[rd] = it[0];
+    ++n;
+#pragma unroll
+    for (int s = 0; s < kStages - 1; ++s) it[s] = it[s + 1];
     rd = rd + 1 == kStages ? 0 : rd + 1;
     wr = wr + 1 == kStages ? 0 : wr + 1;
   }
-  cp_wait<0>();
+  L.wait_all();
+  return n;
 }
 
 // sf_offset in 32-bit arithmetic (scale buffers are < 4 GiB).
@@ -548,12 +735,11 @@ __device__ __forceinline__ EncConsts nv_consts(const AQParams& p, uint32_t gmax_
 }
 
 // Rotate (already done by the caller) -> scales -> codes -> stores of one lane segment.
-template <int FMT>
-__device__ __forceinline__ void encode_seg(const AQParams& p, const Cursor& c, const u64 (&P)[kPairs],
+template <int FMT, typename W>
+__device__ __forceinline__ void encode_seg(const AQParams& p, const W& c, const u64 (&P)[kPairs],
                                            const EncConsts& k, uint32_t& bad) {
-  const int col0 = c.seg * kSeg;
-  if (col0 >= p.Ki || c.row >= p.Mi) return;           // idle lane (after the shuffles)
-  const bool full = col0 + kSeg <= p.Ki;                // else a 16-element tail (K % 32 == 16)
+  if (!c.live(p)) return;                               // idle lane (after the shuffles)
+  const bool full = c.full(p);                          // else a 16-element tail (K % 32 == 16)
   float a0, a1;
   half_amax(P, a0, a1);
   GroupScale s0, s1;
@@ -575,7 +761,7 @@ __device__ __forceinline__ void encode_seg(const AQParams& p, const Cursor& c, c
   uint32_t w[4];
   quantize_seg(P, s0, s1, k.st32, p, w);
 
-  uint8_t* cdst = p.codes + (uint64_t)c.row * p.half_k + (uint32_t)(col0 >> 1);
+  uint8_t* cdst = c.cdst(p);
   if (full) {
     if ((p.Ki & 31) == 0) {
       *reinterpret_cast<uint4*>(cdst) = make_uint4(w[0], w[1], w[2], w[3]);
@@ -587,69 +773,130 @@ __device__ __forceinline__ void encode_seg(const AQParams& p, const Cursor& c, c
     *reinterpret_cast<uint2*>(cdst) = make_uint2(w[0], w[1]);
   }
   if constexpr (FMT == MRFP4_FMT_MXFP4) {
-    p.sf[sf_off32(c.row, c.seg, p.cb)] = (uint8_t)sfc;
+    p.sf[sf_off32(c.row(), c.seg(), p.cb)] = (uint8_t)sfc;
   } else {
     // columns 2*seg, 2*seg+1 share a 16-bit word of the swizzled layout
-    *reinterpret_cast<uint16_t*>(p.sf + sf_off32(c.row, 2 * c.seg, p.cb)) = (uint16_t)sfc;
+    *reinterpret_cast<uint16_t*>(p.sf + sf_off32(c.row(), 2 * c.seg(), p.cb)) = (uint16_t)sfc;
   }
 }
 
+// Per-warp trace stamps (perf experiments), 8 words per warp:
+// [start, end, items | smid << 32, NVFP4 phase-1 end, NVFP4 barrier release, -, -, -].
+struct Trace {
+  unsigned long long* t;
+  __device__ __forceinline__ Trace(const AQParams& p, int warp, int lane)
+      : t(p.trace && lane == 0 ? p.trace + ((int64_t)blockIdx.x * (blockDim.x >> 5) + warp) * 8 : nullptr) {
+    if (t) t[0] = globaltimer();
+  }
+  __device__ __forceinline__ void mark(int i) {
+    if (t) t[i] = globaltimer();
+  }
+  __device__ __forceinline__ void end(int n) {
+    if (t) { t[1] = globaltimer(); t[2] = (unsigned long long)n | ((unsigned long long)smid() << 32); }
+  }
+};
+
 // MXFP4: single pass (group-local scales).
-template <int IN, int HK>
-__global__ void __launch_bounds__(kThreads, 3) k_act_quant_mx(AQParams p) {
-  const int lane = threadIdx.x & 31;
+template <int IN, int HK, typename W, int NW>
+__global__ void __launch_bounds__(NW * 32, 768 / (NW * 32))
+    k_act_quant_mx(const __grid_constant__ CUtensorMap tmx, AQParams p) {
+  __shared__ uint32_t ctr;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   pdl_trigger();
   const EncConsts k;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    pdl_wait();
-    *p.tensor_scale = k.st32;
-  }
+  Trace tr(p, warp, lane);
+  if (threadIdx.x == 0) ctr = 0u;
+  Loader<IN, W> L;
+  init_loader<NW>(L, warp, lane);
+  __syncthreads();
+  pdl_wait();
+  if (blockIdx.x == 0 && threadIdx.x == 0) *p.tensor_scale = k.st32;
+  CtaRange r;
+  r.init(p);
+  Claims cl;
+  cl.init(&ctr, r.cnt, lane);
   uint32_t bad = 0;
-  for_each_seg<IN, 1, false>(p, [] {}, [&](const Cursor& c, uint32_t sbase) {
-    u64 P[kPairs];
-    load_pairs<IN>(sbase, lane, P);
-    if constexpr (HK > 0) fwht<HK>(P, lane, p.pm);
-    encode_seg<MRFP4_FMT_MXFP4>(p, c, P, k, bad);
-  });
+  const int n = run_pipeline<IN, W>(
+      p, &tmx, L, [&] { const int c = cl.next(lane); return c < 0 ? -1 : r.c0 + c; }, nullptr,
+      [&](const W& c, uint32_t sbase) {
+        u64 P[kPairs];
+        load_pairs<IN>(sbase, lane, P);
+        if constexpr (HK > 0) fwht<HK>(P, lane, p.pm);
+        encode_seg<MRFP4_FMT_MXFP4>(p, c, P, k, bad);
+      });
+  tr.end(n);
   if (bad) atomic_or_status(p.status, bad);
   zero_sf_padding(p);
 }
 
 // NVFP4: the whole-tensor scale (quantizers.py:198-200) must be known before any group is
-// encoded.  One persistent launch: phase 1 streams X and reduces max |y| into gmax, a
-// grid barrier (all CTAs are co-resident by construction), then phase 2 walks each warp's
-// items BACKWARDS -- the last kStages items of every lane are still in its SMEM ring, the
-// rest are re-read (mostly L2 hits).  Workspace words: [0] gmax, [1] barrier count,
-// [2] barrier generation, [3] exit count; the last CTA out re-zeroes [0], [3].
-template <int IN, int HK>
-__global__ void __launch_bounds__(kThreads, 3) k_act_quant_nv(AQParams p) {
-  using C = InCfg<IN>;
-  extern __shared__ __align__(128) uint8_t smem_raw[];
+// encoded.  One persistent launch (one CTA per SM, all co-resident by construction):
+//   phase 1 streams X and reduces max |y| into gmax; grid barrier;
+//   phase 2 first encodes the items still held in each warp's ring (the last kStages it
+//   processed), then the CTA's other items, claimed in reverse order (most recently loaded,
+//   so most likely still in L2, first).  A shared bitmap marks the ring-resident items.
+// Workspace words: [0] gmax, [1] barrier count, [2] barrier generation, [3] exit count; the
+// last CTA out re-zeroes [0], [3].
+constexpr int kBitmapWords = 1024;  // ring-resident marks for up to 32768 items per CTA
+
+template <int IN, int HK, typename W, int NW>
+__global__ void __launch_bounds__(NW * 32, 768 / (NW * 32))
+    k_act_quant_nv(const __grid_constant__ CUtensorMap tmx, AQParams p) {
+  constexpr int kStages = InCfg<IN>::kStages;
+  __shared__ uint32_t ctr[2];
+  __shared__ int resident[NW][kMaxStages];
+  __shared__ uint32_t marks[kBitmapWords];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t* ws = p.gmax;
   volatile uint32_t* vgen = ws + 2;
   const uint32_t gen0 = *vgen;  // before arriving: the barrier releases when gen != gen0
+  Trace tr(p, warp, lane);
+  CtaRange r;
+  r.init(p);
+  // Re-encoding the ring-resident items first (no reload) measured faster or equal at every
+  // shape (scripts/k1_ab.py MRFP4_K1_MARKS=0/1), most at decode sizes.
+  const bool use_marks = r.cnt <= 32 * kBitmapWords && p.marks != 0;
+  if (threadIdx.x < 2) ctr[threadIdx.x] = 0u;
+  if (lane < kStages) resident[warp][lane] = -1;
+  if (use_marks)
+    for (int i = threadIdx.x; i < (r.cnt + 31) / 32; i += NW * 32) marks[i] = 0u;
+  Loader<IN, W> L;
+  init_loader<NW>(L, warp, lane);
+  __syncthreads();
+  pdl_wait();
 
   // ---- phase 1: max |y| over the tensor
   float m = 0.f;
-  for_each_seg<IN, 1, false>(p, [] {}, [&](const Cursor&, uint32_t sbase) {
-    u64 P[kPairs];
-    load_pairs<IN>(sbase, lane, P);
-    if constexpr (HK > 0) fwht<HK>(P, lane, p.pm);
-    float a, b;
-    half_amax(P, a, b);   // padding rows / columns were zero-filled
-    m = max3n(a, b, m);
-  });
+  {
+    Claims cl;
+    cl.init(&ctr[0], r.cnt, lane);
+    run_pipeline<IN, W>(
+        p, &tmx, L, [&] { const int c = cl.next(lane); return c < 0 ? -1 : r.c0 + c; }, resident[warp],
+        [&](const W& c, uint32_t sbase) {
+          u64 P[kPairs];
+          load_pairs<IN>(sbase, lane, P);
+          if constexpr (HK > 0) fwht<HK>(P, lane, p.pm);
+          float a, b;
+          half_amax(P, a, b);   // GenWalk: padding rows / columns were zero-filled
+          if (c.live(p)) m = max3n(a, b, m);
+        });
+  }
+  __syncwarp();
+  tr.mark(3);
+  if (use_marks && lane < kStages) {
+    const int it = resident[warp][lane];
+    if (it >= 0) atomicOr(&marks[(it - r.c0) >> 5], 1u << ((it - r.c0) & 31));
+  }
   uint32_t mb = __float_as_uint(m);
   mb = mb > 0x7f800000u ? 0x7fc00000u : mb;  // canonical NaN
   mb = __reduce_max_sync(0xffffffffu, mb);
-  __shared__ uint32_t smax[kWarps];
-  __shared__ uint32_t sg;
+  __shared__ uint32_t smax[NW];
+  __shared__ EncConsts sk;
   if (lane == 0) smax[warp] = mb;
   __syncthreads();
   if (threadIdx.x == 0) {
     uint32_t x = 0;
-    for (int i = 0; i < kWarps; ++i) x = max(x, smax[i]);
+    for (int i = 0; i < NW; ++i) x = max(x, smax[i]);
     if (x) atomicMax(ws, x);
     if (x >= 0x7f800000u) atomic_or_status(p.status, MRFP4_STATUS_NONFINITE);
     // ---- grid barrier
@@ -659,44 +906,53 @@ __global__ void __launch_bounds__(kThreads, 3) k_act_quant_nv(AQParams p) {
       __threadfence();
       atomicAdd(ws + 2, 1u);
     } else {
-      while (*vgen == gen0) __nanosleep(64);
+      uint32_t g;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(ws + 2) : "memory");
+      } while (g == gen0);
     }
     __threadfence();
-    sg = *(volatile uint32_t*)ws;
+    sk = nv_consts(p, *(volatile uint32_t*)ws);  // fp64 divides: once per CTA, not per warp
   }
   __syncthreads();
+  tr.mark(4);
   pdl_trigger();  // only after the barrier: every CTA of this grid is resident by now
-  const EncConsts k = nv_consts(p, sg);
+  const EncConsts k = sk;
   if (blockIdx.x == 0 && threadIdx.x == 0) *p.tensor_scale = k.st32;
 
-  // ---- phase 2: encode, backwards over this warp's items
+  // ---- phase 2: encode
   uint32_t bad = 0;
-  const int64_t gw = (int64_t)blockIdx.x * kWarps + warp, tw = (int64_t)gridDim.x * kWarps;
-  const int64_t i0 = gw * p.items / tw, i1 = (gw + 1) * p.items / tw;
-  const int n = (int)(i1 - i0);
-  if (n > 0) {
-    const uint32_t base =
-        (uint32_t)__cvta_generic_to_shared(smem_raw) + (uint32_t)((warp * kStages * 32 + lane) * C::kLaneBytes);
-    constexpr uint32_t kStride = 32 * C::kLaneBytes;
-    Cursor cp = cursor_at(p, i1 - 1, lane);                    // item n-1 (phase-1 slot (n-1) % kStages)
-    Cursor cr = cp;                                            // reload cursor: item n-1-kStages
-    for (int t = 0; t < kStages; ++t) cursor_step<-1>(p, cr);
-    for (int kk = n - 1; kk >= 0; --kk) {
-      const uint32_t slot = base + (uint32_t)(kk % kStages) * kStride;
-      if (kk < n - kStages) cp_wait<kStages - 1>();           // item kk's reload landed
-      u64 P[kPairs];
-      load_pairs<IN>(slot, lane, P);
-      if constexpr (HK > 0) fwht<HK>(P, lane, p.pm);
-      encode_seg<MRFP4_FMT_NVFP4>(p, cp, P, k, bad);
-      if (kk - kStages >= 0) {                                 // refill this slot with item kk - kStages
-        issue_seg<IN>(p, cr, slot, lane);
-        cursor_step<-1>(p, cr);
+  auto encode = [&](const W& c, uint32_t sbase) {
+    u64 P[kPairs];
+    load_pairs<IN>(sbase, lane, P);
+    if constexpr (HK > 0) fwht<HK>(P, lane, p.pm);
+    encode_seg<MRFP4_FMT_NVFP4>(p, c, P, k, bad);
+  };
+  if (use_marks) {
+#pragma unroll
+    for (int s = 0; s < kStages; ++s) {
+      const int it = resident[warp][s];
+      if (it >= 0) {
+        W c;
+        c.at(p, it, lane);
+        encode(c, L.slot(s));
       }
-      cp_commit();
-      cursor_step<-1>(p, cp);
     }
-    cp_wait<0>();
   }
+  Claims cl;
+  cl.init(&ctr[1], r.cnt, lane);
+  const int n = run_pipeline<IN, W>(
+      p, &tmx, L,
+      [&] {
+        while (true) {
+          const int c = cl.next(lane);
+          if (c < 0) return -1;
+          const int off = r.cnt - 1 - c;
+          if (!use_marks || !((marks[off >> 5] >> (off & 31)) & 1u)) return r.c0 + off;
+        }
+      },
+      nullptr, encode);
+  tr.end(n);
   if (bad) atomic_or_status(p.status, bad);
   zero_sf_padding(p);
   // Last CTA out re-arms gmax for the next call (every CTA read it before the barrier released).
@@ -720,21 +976,22 @@ __global__ void __launch_bounds__(kThreads, 3) k_act_quant_nv(AQParams p) {
 // Off the hot path (quantized_linear never asks for it).
 // ---------------------------------------------------------------------------
 template <int IN, int FMT, int HK>
-__global__ void __launch_bounds__(kThreads) k_quant_metrics(AQParams p, double* acc) {
+__global__ void __launch_bounds__(kMetricWarps * 32) k_quant_metrics(AQParams p, double* acc) {
   using C = InCfg<IN>;
   constexpr int G = FMT == MRFP4_FMT_MXFP4 ? 32 : 16;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const float ts = *p.tensor_scale;
   double e2 = 0.0, x2 = 0.0, top = 0.0;
-  const int64_t gw = (int64_t)blockIdx.x * kWarps + warp, tw = (int64_t)gridDim.x * kWarps;
+  const int64_t gw = (int64_t)blockIdx.x * kMetricWarps + warp, tw = (int64_t)gridDim.x * kMetricWarps;
   for (int64_t item = gw; item < p.items; item += tw) {
-    const Cursor c = cursor_at(p, item, lane);
-    const int col0 = c.seg * kSeg;
-    const bool live = col0 < p.Ki && c.row < p.Mi;
+    GenWalk c;
+    c.at(p, item, lane);
+    const int col0 = c.seg() * kSeg;
+    const bool live = c.live(p);
     const int nvalid = live ? min(kSeg, p.Ki - col0) : 0;
     uint32_t w[kSeg * C::kEs / 4];
     const uint32_t* src = reinterpret_cast<const uint32_t*>(static_cast<const char*>(p.x) +
-                                                            ((uint64_t)c.row * p.ldx + (uint32_t)col0) * C::kEs);
+                                                            ((uint64_t)c.row() * p.ldx + (uint32_t)col0) * C::kEs);
 #pragma unroll
     for (int j = 0; j < kSeg * C::kEs / 4; ++j) w[j] = (j * 4 < nvalid * C::kEs) ? src[j] : 0u;
     u64 P[kPairs];
@@ -751,10 +1008,10 @@ __global__ void __launch_bounds__(kThreads) k_quant_metrics(AQParams p, double* 
     }
     if constexpr (HK > 0) fwht<HK>(P, lane, p.pm);
     if (!live) continue;
-    const uint8_t* cb = p.codes + (uint64_t)c.row * p.half_k + (uint32_t)(col0 >> 1);
+    const uint8_t* cb = p.codes + (uint64_t)c.row() * p.half_k + (uint32_t)(col0 >> 1);
     for (int g0 = 0; g0 < nvalid; g0 += G) {
       const int gcol = (col0 + g0) / G;
-      const uint32_t scode = p.sf[sf_off32(c.row, gcol, p.cb)];
+      const uint32_t scode = p.sf[sf_off32(c.row(), gcol, p.cb)];
       const double dec = FMT == MRFP4_FMT_MXFP4 ? ldexp(1.0, (int)scode - 127) : (double)e4m3_value(scode);
       const double eff = (double)ts * dec;
       double best = -1.0, yt = 0.0, qt = 0.0;
@@ -788,6 +1045,12 @@ __global__ void __launch_bounds__(kThreads) k_quant_metrics(AQParams p, double* 
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
+// Perf-experiment knobs (environment, read per call; unset in production).
+int knob(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::atoi(v) : dflt;
+}
+
 int num_sms() {
   static int n = 0;
   if (n == 0) {
@@ -800,8 +1063,8 @@ int num_sms() {
 }
 
 // One CTA set per SM that the occupancy calculator allows (cached per kernel).
-template <auto Kern>
-int launch_persistent(int smem, const AQParams& p, cudaStream_t s) {
+template <auto Kern, int NW>
+int launch_persistent(int smem, const CUtensorMap& tm, const AQParams& p, cudaStream_t s) {
   static std::once_flag once;
   static int per_sm = -1;
   std::call_once(once, [&] {
@@ -809,20 +1072,54 @@ int launch_persistent(int smem, const AQParams& p, cudaStream_t s) {
     // Max-shared carveout (the GEMM's too), so K1 -> K2 -> K1 never reconfigures L1/SMEM.
     cudaFuncSetAttribute(Kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
     if (cudaFuncSetAttribute(Kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) == cudaSuccess &&
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, Kern, kThreads, smem) == cudaSuccess)
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, Kern, NW * 32, smem) == cudaSuccess)
       per_sm = std::max(n, 1);
   });
   if (per_sm < 0) return MRFP4_ECUDA;
-  const int64_t need = ceil_div(p.items, kWarps);
+  const int64_t need = ceil_div(p.items, NW);
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)per_sm * num_sms()));
-  return launch_pdl(Kern, dim3(grid), dim3(kThreads), smem, s, p) == cudaSuccess ? MRFP4_OK : MRFP4_ECUDA;
+  return launch_pdl(Kern, dim3(grid), dim3(NW * 32), smem, s, tm, p) == cudaSuccess ? MRFP4_OK : MRFP4_ECUDA;
+}
+
+// FlatWalk's TMA view of X: [total_segs rows][one segment = kLaneBytes] bytes, box = one
+// item (32 segments), swizzled like the cp.async ring (64 B rows: SWIZZLE_64B, 128 B: 128B).
+template <int IN>
+bool make_segment_map(CUtensorMap* tm, const AQParams& p) {
+  using C = InCfg<IN>;
+  auto encode = tensor_map_encoder();
+  if (!encode) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)C::kLaneBytes, (cuuint64_t)p.total_segs};
+  cuuint64_t strides[1] = {(cuuint64_t)C::kLaneBytes};
+  cuuint32_t box[2] = {(cuuint32_t)C::kLaneBytes, 32};
+  cuuint32_t estr[2] = {1, 1};
+  return encode(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(p.x), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE,
+                C::kLaneBytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int IN, int FMT, int HK, int NW>
+int launch_nw(const AQParams& p, const CUtensorMap& tm, cudaStream_t s) {
+  constexpr int smem = InCfg<IN>::smem(NW);
+  if constexpr (FMT == MRFP4_FMT_NVFP4) {
+    if (p.nseg) return launch_persistent<k_act_quant_nv<IN, HK, FlatWalk, NW>, NW>(smem, tm, p, s);
+    return launch_persistent<k_act_quant_nv<IN, HK, GenWalk, NW>, NW>(smem, tm, p, s);
+  }
+  if (p.nseg) return launch_persistent<k_act_quant_mx<IN, HK, FlatWalk, NW>, NW>(smem, tm, p, s);
+  return launch_persistent<k_act_quant_mx<IN, HK, GenWalk, NW>, NW>(smem, tm, p, s);
 }
 
 template <int IN, int FMT, int HK>
 int launch_hk(const AQParams& p, cudaStream_t s) {
-  constexpr int smem = InCfg<IN>::kSmem;
-  if constexpr (FMT == MRFP4_FMT_NVFP4) return launch_persistent<k_act_quant_nv<IN, HK>>(smem, p, s);
-  return launch_persistent<k_act_quant_mx<IN, HK>>(smem, p, s);
+  CUtensorMap tm;
+  memset(&tm, 0, sizeof(tm));
+  if (p.nseg && !make_segment_map<IN>(&tm, p)) return MRFP4_ECUDA;
+  // MXFP4: one 24-warp CTA per SM (the SM's warps share one work queue; best at large M).
+  // NVFP4: three 8-warp CTAs per SM (its two phases and grid barrier run better in smaller
+  // CTAs -- scripts/k1_warps.sh).
+  const int nw = knob(FMT == MRFP4_FMT_NVFP4 ? "MRFP4_K1_NVWARPS" : "MRFP4_K1_MXWARPS",
+                      FMT == MRFP4_FMT_NVFP4 ? 8 : 24);
+  return nw == 8 ? launch_nw<IN, FMT, HK, 8>(p, tm, s) : launch_nw<IN, FMT, HK, 24>(p, tm, s);
 }
 
 template <int IN, int FMT>
@@ -847,8 +1144,12 @@ int dispatch_fmt(const AQParams& p, int fmt, int hk, cudaStream_t s) {
 
 // Host launcher; arguments validated by the C-ABI layer (capi.cu).
 namespace {
+
+unsigned long long* g_k1_trace = nullptr;
+// flat_ok: the caller's kernel supports FlatWalk (chosen when rows are contiguous, K % 32 == 0,
+// K >= 1024 and the segment count fits 32 bits); p.nseg != 0 marks the flat walk.
 AQParams make_params(const void* x, int64_t M, int64_t K, int64_t ldx, int fmt, int hk, uint8_t* codes, uint8_t* sf,
-                     float* tensor_scale, uint32_t* status, void* workspace) {
+                     float* tensor_scale, uint32_t* status, void* workspace, bool flat_ok) {
   AQParams p;
   p.x = x;
   p.M = M;
@@ -872,6 +1173,19 @@ AQParams make_params(const void* x, int64_t M, int64_t K, int64_t ldx, int fmt, 
   p.nchunk = (int)ceil_div(nseg, 1 << lb);
   p.seg_span = p.nchunk << lb;
   p.items = ceil_div(M, 32 >> lb) * p.nchunk;
+  p.nseg = 0;
+  p.total_segs = 0;
+  p.trace = g_k1_trace;
+  p.x_bytes = 0;
+  p.marks = -1;
+  if (flat_ok && ldx == K && K % kSeg == 0 && K >= 32 * kSeg && M * (K / kSeg) < (int64_t(1) << 31) &&
+      !knob("MRFP4_K1_GENWALK", 0)) {
+    p.nseg = (int)(K / kSeg);
+    p.total_segs = (uint32_t)(M * (K / kSeg));
+    p.items = ceil_div((int64_t)p.total_segs, 32);
+  }
+  const int64_t d = p.nseg ? p.nseg : p.nchunk;
+  p.div_m = d > 1 ? (uint32_t)(((uint64_t(1) << 32) + (uint64_t)d - 1) / (uint64_t)d) : 0u;
   p.Mi = (int)M;
   p.Ki = (int)K;
   p.half_k = (uint32_t)(K / 2);
@@ -890,7 +1204,9 @@ AQParams make_params(const void* x, int64_t M, int64_t K, int64_t ldx, int fmt, 
 int launch_act_quant(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ldx, int fmt, int hk,
                      uint8_t* codes, uint8_t* sf, float* tensor_scale, uint32_t* status,
                      void* workspace, cudaStream_t s) {
-  const AQParams p = make_params(x, M, K, ldx, fmt, hk, codes, sf, tensor_scale, status, workspace);
+  AQParams p = make_params(x, M, K, ldx, fmt, hk, codes, sf, tensor_scale, status, workspace, true);
+  p.x_bytes = (uint64_t)M * (uint64_t)K * (x_dtype == MRFP4_DT_F32 ? 4u : 2u);
+  p.marks = knob("MRFP4_K1_MARKS", -1);
   int rc;
   switch (x_dtype) {
     case MRFP4_DT_BF16: rc = dispatch_fmt<MRFP4_DT_BF16>(p, fmt, hk, s); break;
@@ -906,10 +1222,10 @@ int launch_quant_metrics(const void* x, int x_dtype, int64_t M, int64_t K, int64
                          const uint8_t* codes, const uint8_t* sf, const float* tensor_scale, double* acc,
                          cudaStream_t s) {
   const AQParams p = make_params(x, M, K, ldx, fmt, hk, const_cast<uint8_t*>(codes), const_cast<uint8_t*>(sf),
-                                 const_cast<float*>(tensor_scale), nullptr, nullptr);
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(p.items, kWarps), 4 * num_sms()));
+                                 const_cast<float*>(tensor_scale), nullptr, nullptr, false);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(p.items, kMetricWarps), 4 * num_sms()));
   auto go = [&](auto kern) {
-    kern<<<grid, kThreads, 0, s>>>(p, acc);
+    kern<<<grid, kMetricWarps * 32, 0, s>>>(p, acc);
     return cudaPeekAtLastError() == cudaSuccess ? MRFP4_OK : MRFP4_ECUDA;
   };
 #define MRFP4_MCASE(IN, FMT, HK) \
@@ -926,3 +1242,6 @@ int launch_quant_metrics(const void* x, int x_dtype, int64_t M, int64_t K, int64
 }
 
 }  // namespace mrfp4
+
+// Perf experiments only: per-warp timeline stamps (see Trace).
+extern "C" void mrfp4_debug_k1_trace(unsigned long long* buf) { mrfp4::g_k1_trace = buf; }

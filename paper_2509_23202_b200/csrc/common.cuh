@@ -15,6 +15,16 @@ namespace mrfp4 {
 // layout): 128-row x 4-column atoms of 512 bytes, atoms K-contiguous.
 // offset(r, c) = ((r/128)*ceil(C/4) + c/4)*512 + (r%32)*16 + ((r/32)%4)*4 + c%4
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ uint32_t smid() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
 __host__ __device__ __forceinline__ int64_t sf_offset(int64_t r, int64_t c, int64_t col_blocks) {
   return ((r >> 7) * col_blocks + (c >> 2)) * 512 + (r & 31) * 16 + ((r >> 5) & 3) * 4 + (c & 3);
 }

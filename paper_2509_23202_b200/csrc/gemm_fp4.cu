@@ -814,6 +814,10 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
   return fn;
 }
 
+}  // namespace
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() { return get_encode_fn(); }
+namespace {
+
 bool make_code_map(CUtensorMap* tm, const uint8_t* ptr, int64_t rows, int64_t K, int box_rows) {
   auto encode = get_encode_fn();
   if (!encode) return false;

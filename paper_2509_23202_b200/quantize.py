@@ -75,7 +75,7 @@ class GpuQuantResult:
     codes: torch.Tensor            # uint8 [rows, cols // 2]
     sf: torch.Tensor               # uint8, swizzled 128x4-atom layout
     tensor_scale_dev: torch.Tensor  # float32 [1]
-    scratch: torch.Tensor          # int32 [8]: [0] status bits, [4:] workspace
+    scratch: torch.Tensor          # int32 [12]: [0] status bits, [4:12] act-quant workspace (32 B)
     source: torch.Tensor | None = None   # the input X (for the lazily computed metrics)
     _metrics: tuple | None = None
 
@@ -155,7 +155,7 @@ def act_quant_into(X: torch.Tensor, fmt: int, had_k: int, codes: torch.Tensor, s
     L = _lib.lib()
     _lib.check(L.mrfp4_act_quant(_lib.ptr(X), _DT[X.dtype], M, K, X.stride(0), fmt, had_k,
                                  _lib.ptr(codes), _lib.ptr(sf), _lib.ptr(ts), _lib.ptr(scratch),
-                                 _lib.ptr(scratch) + 16, 16, _lib.stream_ptr(torch, X.device)))
+                                 _lib.ptr(scratch) + 16, 32, _lib.stream_ptr(torch, X.device)))
 
 
 def alloc_result(M: int, K: int, fmt: int, had_k: int, device) -> GpuQuantResult:
@@ -166,7 +166,7 @@ def alloc_result(M: int, K: int, fmt: int, had_k: int, device) -> GpuQuantResult
         torch.empty((M, K // 2), dtype=torch.uint8, device=device),
         torch.empty(sfb, dtype=torch.uint8, device=device),
         torch.empty(1, dtype=torch.float32, device=device),
-        torch.zeros(8, dtype=torch.int32, device=device))
+        torch.zeros(12, dtype=torch.int32, device=device))
 
 
 def quantize_rtn(X, spec, policy=None, transform=None, *, check: bool = True) -> GpuQuantResult:

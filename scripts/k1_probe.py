@@ -8,18 +8,18 @@ from paper_2509_23202_b200.quantize import alloc_result, act_quant_into
 flush = torch.empty(256 * 2**20, dtype=torch.uint8, device="cuda")
 peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")))["hbm_gbs"]
 
-def timeit(fn, iters=30, warm=5):
+def timeit(fn, iters=100, warm=5):
     """Median device time; all iterations enqueued before one sync (the host runs ahead)."""
     for _ in range(warm):
         fn()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(iters)]
     torch.cuda.synchronize()
     for s, e in ev:
-        flush.zero_()
+        flush.zero_(); flush.sum(dtype=torch.int32)
         s.record(); fn(); e.record()
     torch.cuda.synchronize()
-    ts = sorted(s.elapsed_time(e) for s, e in ev)
-    return ts[len(ts) // 2] * 1e-3
+    ts = [s.elapsed_time(e) for s, e in ev]
+    return sum(ts) / len(ts) * 1e-3  # mean: event times are quantized (~2 us steps)
 
 for M, K, fmt, k in [(2048, 14336, 0, 32), (2048, 14336, 1, 16), (2048, 8192, 1, 16), (2048, 28672, 0, 32),
                      (2048, 28672, 1, 16), (8192, 28672, 0, 32), (2048, 5120, 1, 128), (2048, 25600, 1, 128),

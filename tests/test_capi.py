@@ -43,7 +43,8 @@ def test_sizes():
     assert L.mrfp4_sf_bytes(1, 1) == 512
     assert L.mrfp4_sf_bytes(129, 5) == 256 * 8
     assert L.mrfp4_sf_bytes(2048, 448) == 2048 * 448
-    assert L.mrfp4_act_quant_workspace(16, 4096, 1) >= 4
+    assert L.mrfp4_act_quant_workspace(16, 4096, 1) == 16
+    assert L.mrfp4_act_quant_workspace(2048, 14336, 0) == 0
 
 
 @pytest.mark.parametrize("args,msg", [

@@ -41,7 +41,7 @@ def run_gemm(A, W, out_dtype=torch.float32):
     a = P.prepare_weight(to_mfp(A))       # same device layout for activations
     w = P.prepare_weight(to_mfp(W))
     act = P.GpuQuantResult(a.fmt, a.N, a.K, 0, a.codes, a.sf, a.tensor_scale_dev,
-                           torch.zeros(8, dtype=torch.int32, device="cuda"))
+                           torch.zeros(12, dtype=torch.int32, device="cuda"))
     out = torch.empty((A.rows, W.rows), dtype=out_dtype, device="cuda")
     P.gemm(act, w, out)
     torch.cuda.synchronize()
