@@ -154,9 +154,13 @@ def main():
     ap.add_argument("--config", default="c1", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--M", type=int, default=0, help="override the config's token count (sweeps)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = CONFIGS[args.config]
+    if args.M:
+        cfg = (cfg[0].rsplit(",", 2)[0] + f", {args.M} tokens," + cfg[0].rsplit(",", 1)[1],
+               args.M) + tuple(cfg[2:])
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -198,7 +202,9 @@ def main():
         flush_w.zero_()                    # write a buffer larger than L2 (126 MB) ...
         flush_r.sum(dtype=torch.int32)     # ... then read another: L2 left clean, none of our data
 
-    launches_per_step = (1 if fmt == "mxfp4" else 2) + 1   # K1 (NVFP4: tensor-max pass + encode pass) + K2
+    # K1 (one launch for both formats) + K2 (+ the split-K reduce for small M)
+    from paper_2509_23202_b200 import _lib
+    launches_per_step = 2 + (1 if _lib.lib().mrfp4_gemm_workspace(M, w.N, K, w.fmt) > 0 else 0)
 
     def step():
         act_quant_into(x, w.fmt, had, a.codes, a.sf, a.tensor_scale_dev, a.scratch)
