@@ -278,12 +278,11 @@ def main():
         ne = min(args.steps, 20)
 
         def e2e_step():
-            xd.copy_(xh, non_blocking=True)
             if world > 1:
-                yy = P.quantized_linear_sharded(xd, w)
-            else:
-                yy = P.quantized_linear(xd, w)
-            yh.copy_(yy, non_blocking=True)
+                xd.copy_(xh, non_blocking=True)
+                yh.copy_(P.quantized_linear_sharded(xd, w), non_blocking=True)
+            else:   # public host-buffer API: H2D, K1 + K2 and D2H pipelined over row chunks
+                P.quantized_linear_host(xh, w, out=yh)
 
         for _ in range(3):
             e2e_step()

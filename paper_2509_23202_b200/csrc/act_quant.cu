@@ -968,6 +968,543 @@ __global__ void __launch_bounds__(NW * 32, 768 / (NW * 32))
 }
 
 // ---------------------------------------------------------------------------
+// K1m: the rotation on the tensor cores (bf16 / f16 input, contiguous rows, K % 32 == 0,
+// K >= 1024, k in {16, 32, 64, 128}).
+//
+// Per warp sub-item: 32 consecutive 32-element segments (2 KB of bf16) of the flattened X,
+// one 32 x 32 tile.  Y = X_tile . H32' by 16 mma.sync.m16n8k16 (fp32 accumulate; +-1
+// operands, so the products are exact and each output is the fp32 sum the butterfly would
+// produce -- scripts/hmma_probe.cu: no less exact than the FWHT), where H32' is H32 (or
+// diag(H16, H16)) with its columns permuted so that lane (g, t) = (lane / 4, lane % 4)
+// receives output elements 8t .. 8t+7 of segments 8j + g, j = 0..3 ("slot" j): 4 f32 pairs
+// per slot, i.e. one 32-bit word of codes.  k = 64 / 128 add the H2 / H4 factor across
+// segments (8j + g) ^ 1 / ^ 2, i.e. lanes xor 4 / 8.
+// The group absmax is a reduce-scatter over the lanes sharing a group (MXFP4: the quad,
+// lane t ends with segment 8t + g; NVFP4: the lane pair, each lane with two groups), so
+// every scale code is computed once; the element multipliers go back by shuffles.
+// Replaces ~80 FADD2/FFMA2 + 32 unpack instructions per lane segment with 16 HMMA per
+// warp tile (0.5 HMMA/clk/SM measured, ~3 us of tensor time at c1).
+// ---------------------------------------------------------------------------
+template <int IN>
+__device__ __forceinline__ void hmma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  if constexpr (IN == MRFP4_DT_BF16) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+  } else {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+  }
+}
+
+__device__ __forceinline__ void ldsm_x4(uint32_t saddr, uint32_t (&a)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(a[0]), "=r"(a[1]), "=r"(a[2]), "=r"(a[3])
+               : "r"(saddr));
+}
+
+__device__ __forceinline__ float maxn(float a, float b) {
+  float r;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+
+// B fragments of the permuted Hadamard (constant per lane): b[(kt * 4 + nt) * 2 + r] holds
+// rows k = 16 kt + 2t + 8r, k + 1 of column n = g of n-tile nt, which is output element
+// e = 8 (g >> 1) + 2 nt + (g & 1).  Entry (-1)^popc(k & e) (k = 16: (-1)^popc(k & e & 15) on
+// the two diagonal 16 x 16 blocks, zero off them).
+template <int IN, int HK>
+__device__ __forceinline__ void hadamard_frags(int lane, uint32_t (&b)[16]) {
+  const int g = lane >> 2, t = lane & 3;
+  const uint32_t one = IN == MRFP4_DT_BF16 ? 0x3F80u : 0x3C00u;
+  const uint32_t neg = 0x8000u;
+#pragma unroll
+  for (int kt = 0; kt < 2; ++kt)
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int k0 = 16 * kt + 2 * t + 8 * r;
+        const int e = 8 * (g >> 1) + 2 * nt + (g & 1);
+        uint32_t v = 0;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int k = k0 + h;
+          const bool live = HK != 16 || (k >> 4) == (e >> 4);
+          const uint32_t x = live ? (one | ((__popc(k & e & (HK == 16 ? 15 : 31)) & 1) ? neg : 0u)) : 0u;
+          v |= x << (16 * h);
+        }
+        b[(kt * 4 + nt) * 2 + r] = v;
+      }
+}
+
+// ldmatrix addresses (bytes from the tile base) of lane's rows for (mt, kt) = (i / 2, i % 2):
+// matrix q = lane / 8 -> rows 16 mt + 8 (q & 1) + lane % 8, 16-B chunk 2 kt + (q >> 1), under
+// the TMA 64-B swizzle (chunk ^= (row >> 1) & 3).  The 8 rows of a matrix are consecutive
+// segments: conflict-free.
+__device__ __forceinline__ void ldsm_offsets(int lane, uint32_t (&off)[4]) {
+  const int q = lane >> 3, r8 = lane & 7;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int mt = i >> 1, kt = i & 1;
+    const int seg = 16 * mt + 8 * (q & 1) + r8;
+    const int chunk = 2 * kt + (q >> 1);
+    off[i] = (uint32_t)(seg * 64 + ((chunk ^ ((seg >> 1) & 3)) * 16));
+  }
+}
+
+// 32 x 32 tile at `sbase` -> P[j][nt] = output elements (8t + 2nt, 8t + 2nt + 1) of segment 8j + g.
+template <int IN, int HK>
+__device__ __forceinline__ void rotate_tile(uint32_t sbase, const uint32_t (&off)[4], const uint32_t (&b)[16],
+                                            int lane, u64 (&P)[4][4]) {
+  float c[2][4][4];
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int z = 0; z < 4; ++z) c[mt][nt][z] = 0.f;
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int kt = 0; kt < 2; ++kt) {
+      uint32_t a[4];
+      ldsm_x4(sbase + off[2 * mt + kt], a);
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) hmma16816<IN>(c[mt][nt], a, b[(kt * 4 + nt) * 2], b[(kt * 4 + nt) * 2 + 1]);
+    }
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+      P[2 * mt][nt] = pk(c[mt][nt][0], c[mt][nt][1]);
+      P[2 * mt + 1][nt] = pk(c[mt][nt][2], c[mt][nt][3]);
+    }
+  // Segment-index bits 0 / 1 (k = 64 / 128) live in lane bits 2 / 3.
+  if constexpr (HK >= 64) {
+    const float s = (lane & 4) ? -1.f : 1.f;
+    const u64 sg = pk(s, s);
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) P[j][nt] = fma2(sg, P[j][nt], __shfl_xor_sync(0xffffffffu, P[j][nt], 4));
+  }
+  if constexpr (HK >= 128) {
+    const float s = (lane & 8) ? -1.f : 1.f;
+    const u64 sg = pk(s, s);
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) P[j][nt] = fma2(sg, P[j][nt], __shfl_xor_sync(0xffffffffu, P[j][nt], 8));
+  }
+}
+
+__device__ __forceinline__ float slot_amax(const u64 (&Pj)[4]) {
+  const float a = amax3(lo_of(Pj[0]), hi_of(Pj[0]), lo_of(Pj[1]));
+  const float b = amax3(hi_of(Pj[1]), lo_of(Pj[2]), hi_of(Pj[2]));
+  const float c = amax3(lo_of(Pj[3]), hi_of(Pj[3]), 0.f);
+  return max3n(a, b, c);
+}
+
+// 8 elements -> one word of E2M1 codes, rounded twice (u * (1 +- 2^-18)); nibbles that
+// disagree are re-decided exactly by the caller.
+__device__ __forceinline__ uint32_t quant_slot(const u64 (&Pj)[4], float f, uint32_t& diff) {
+  constexpr float kEps = 3.814697265625e-06f;  // 2^-18
+  const float fh = f * (1.f + kEps), fl = f * (1.f - kEps);
+  float uh[8], ul[8];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const u64 a = mul2(Pj[t], pk(fh, fh)), b = mul2(Pj[t], pk(fl, fl));
+    uh[2 * t] = lo_of(a); uh[2 * t + 1] = hi_of(a);
+    ul[2 * t] = lo_of(b); ul[2 * t + 1] = hi_of(b);
+  }
+  const uint32_t w = cvt_e2m1x8(uh);
+  diff = w ^ cvt_e2m1x8(ul);
+  return w;
+}
+
+// Decoded group scale from its code (exact in fp32), as mx_group_scale / nv_group_scale.
+template <int FMT>
+__device__ __forceinline__ float dec_of(uint32_t code) {
+  if constexpr (FMT == MRFP4_FMT_MXFP4) {
+    const int e = (int)code - 127;
+    return __uint_as_float(e >= -126 ? (uint32_t)(e + 127) << 23 : 0x00400000u);
+  } else {
+    return e4m3_value(code);
+  }
+}
+
+// Rare: re-decide the nibbles of `w` flagged in `redo` (all when slow) exactly (quantizers.py:213).
+template <int FMT>
+__device__ __noinline__ uint32_t redo_slot(uint32_t w, uint32_t redo, bool slow, const float (&v)[8], double c64,
+                                           float ts, uint32_t code) {
+  const float dec = dec_of<FMT>(code);
+  for (int e = 0; e < 8; ++e) {
+    if (slow || ((redo >> (4 * e)) & 0xFu)) {
+      const uint32_t c = fp4_code_exact(v[e], c64, ts, dec);
+      w = (w & ~(0xFu << (4 * e))) | (c << (4 * e));
+    }
+  }
+  return w;
+}
+
+// Row / column of global segment s (flat walk).
+__device__ __forceinline__ void seg_rc(const AQParams& p, uint32_t s, uint32_t& row, uint32_t& col) {
+  row = fast_div(s, (uint32_t)p.nseg, p.div_m);
+  col = s - row * (uint32_t)p.nseg;
+}
+
+// Encode one 32-segment tile whose first global segment is s0.  Returns nothing; ORs status bits.
+template <int FMT>
+__device__ __forceinline__ void encode_tile(const AQParams& p, const EncConsts& k, const u64 (&P)[4][4], uint32_t s0,
+                                            int lane, uint32_t& bad) {
+  const int g = lane >> 2, t = lane & 3;
+  float m[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) m[j] = slot_amax(P[j]);
+  float f[4];
+  uint32_t codes_own, codes_oth;  // FMT-specific packing of the 4 slots' codes (slow path)
+  bool slow;
+  if constexpr (FMT == MRFP4_FMT_MXFP4) {
+    // reduce-scatter over the quad: lane t ends with the max of slot t (segment 8t + g)
+    const bool hi2 = t & 2, hi1 = t & 1;
+    float k0 = hi2 ? m[2] : m[0], k1 = hi2 ? m[3] : m[1];
+    const float s0v = hi2 ? m[0] : m[2], s1v = hi2 ? m[1] : m[3];
+    k0 = maxn(k0, __shfl_xor_sync(0xffffffffu, s0v, 2));
+    k1 = maxn(k1, __shfl_xor_sync(0xffffffffu, s1v, 2));
+    const float a = maxn(hi1 ? k1 : k0, __shfl_xor_sync(0xffffffffu, hi1 ? k0 : k1, 1));
+    if (__float_as_uint(a) >= 0x7f800000u) bad |= MRFP4_STATUS_NONFINITE;
+    const GroupScale gs = mx_group_scale(a, p);
+    const int qb = lane & ~3;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) f[j] = __shfl_sync(0xffffffffu, gs.f, qb | j);
+    uint32_t cw = gs.code << (8 * t);
+    cw |= __shfl_xor_sync(0xffffffffu, cw, 1);
+    cw |= __shfl_xor_sync(0xffffffffu, cw, 2);
+    codes_own = cw;
+    codes_oth = 0;
+    slow = __any_sync(0xffffffffu, gs.slow_all);
+    const uint32_t s = s0 + 8u * (uint32_t)t + (uint32_t)g;
+    if (s < p.total_segs) {
+      uint32_t row, col;
+      seg_rc(p, s, row, col);
+      p.sf[sf_off32(row, col, p.cb)] = (uint8_t)gs.code;
+    }
+  } else {
+    // reduce-scatter over the lane pair: even lanes keep slots 0, 1, odd lanes slots 2, 3
+    const bool odd = t & 1;
+    float k0 = odd ? m[2] : m[0], k1 = odd ? m[3] : m[1];
+    const float s0v = odd ? m[0] : m[2], s1v = odd ? m[1] : m[3];
+    k0 = maxn(k0, __shfl_xor_sync(0xffffffffu, s0v, 1));
+    k1 = maxn(k1, __shfl_xor_sync(0xffffffffu, s1v, 1));
+    const GroupScale g0 = nv_group_scale(k0, p, k.kenc, k.knv, k.st32, k.st64, k.zero_code);
+    const GroupScale g1 = nv_group_scale(k1, p, k.kenc, k.knv, k.st32, k.st64, k.zero_code);
+    if (__float_as_uint(k0) >= 0x7f800000u || __float_as_uint(k1) >= 0x7f800000u) bad |= MRFP4_STATUS_NONFINITE;
+    const float o0 = __shfl_xor_sync(0xffffffffu, g0.f, 1), o1 = __shfl_xor_sync(0xffffffffu, g1.f, 1);
+    f[0] = odd ? o0 : g0.f; f[1] = odd ? o1 : g1.f;
+    f[2] = odd ? g0.f : o0; f[3] = odd ? g1.f : o1;
+    const uint32_t cw = g0.code | (g1.code << 8);
+    codes_own = cw;
+    codes_oth = __shfl_xor_sync(0xffffffffu, cw, 1);
+    slow = __any_sync(0xffffffffu, g0.slow_all | g1.slow_all);
+    const uint32_t gi = (uint32_t)(t >> 1);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t code = h ? g1.code : g0.code;
+      const uint32_t s = s0 + 8u * (uint32_t)(2 * (t & 1) + h) + (uint32_t)g;
+      if (s < p.total_segs) {
+        if (code == 0) bad |= MRFP4_STATUS_SCALE_UNDERFLOW;
+        uint32_t row, col;
+        seg_rc(p, s, row, col);
+        p.sf[sf_off32(row, 2 * col + gi, p.cb)] = (uint8_t)code;
+      }
+    }
+  }
+  uint32_t w[4], dif[4], any = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    w[j] = quant_slot(P[j], f[j], dif[j]);
+    any |= dif[j];
+  }
+  if (any | (uint32_t)slow) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (dif[j] | (uint32_t)slow) {
+        float v[8];
+#pragma unroll
+        for (int z = 0; z < 4; ++z) { v[2 * z] = lo_of(P[j][z]); v[2 * z + 1] = hi_of(P[j][z]); }
+        uint32_t code;
+        if constexpr (FMT == MRFP4_FMT_MXFP4) {
+          code = (codes_own >> (8 * j)) & 0xFFu;
+        } else {
+          const bool mine = (j >> 1) == (t & 1);
+          code = ((mine ? codes_own : codes_oth) >> (8 * (j & 1))) & 0xFFu;
+        }
+        w[j] = redo_slot<FMT>(w[j], dif[j], slow, v, p.c64, k.st32, code);
+      }
+    }
+  }
+  uint32_t* cdst = reinterpret_cast<uint32_t*>(p.codes) + (uint64_t)s0 * 4u + (uint32_t)(4 * g + t);
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    if (s0 + 8u * j + (uint32_t)g < p.total_segs) cdst[32 * j] = fix_neg_zero(w[j]);
+}
+
+// Per-warp TMA ring of kStages items of U tiles (U * 2 KB) for K1m.
+template <int U, int S>
+struct MRing {
+  static constexpr uint32_t kItemBytes = 32u * U * 64u;
+  uint32_t base, bars, ph;
+  int lane;
+  __device__ __forceinline__ void init(uint32_t ring, uint32_t bar_addr, int lane_) {
+    lane = lane_;
+    base = ring;
+    bars = bar_addr;
+    ph = 0;
+    if (lane == 0) {
+#pragma unroll
+      for (int s = 0; s < S; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bars + 8 * s));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+  }
+  __device__ __forceinline__ uint32_t slot(int s) const { return base + (uint32_t)s * kItemBytes; }
+  __device__ __forceinline__ void issue(const CUtensorMap* tm, int item, int s) {
+    if (lane == 0) {
+      const uint32_t bar = bars + 8 * s;
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(kItemBytes) : "memory");
+      asm volatile(
+          "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+          " [%0], [%1, {%3, %4}], [%2];" ::"r"(slot(s)),
+          "l"(reinterpret_cast<uint64_t>(tm)), "r"(bar), "r"(0), "r"(item * 32 * U)
+          : "memory");
+    }
+  }
+  __device__ __forceinline__ void wait(int s) {
+    const uint32_t par = (ph >> s) & 1u;
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n\t}" ::"r"(bars + 8 * s),
+        "r"(par)
+        : "memory");
+    ph ^= 1u << s;
+  }
+  __device__ __forceinline__ void release() {
+    __syncwarp();
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+};
+
+// Issue item j + S - 1 while item j is processed; item j of the walk sits in slot j % S.
+template <int U, int S, typename N, typename F>
+__device__ __forceinline__ int run_ring(const CUtensorMap* tm, MRing<U, S>& R, N&& next, int* resident, int lane,
+                                        F&& body) {
+  int it[S];
+  R.release();
+#pragma unroll
+  for (int s = 0; s < S - 1; ++s) {
+    it[s] = next();
+    if (it[s] >= 0) R.issue(tm, it[s], s);
+  }
+  int rd = 0, wr = S - 1, n = 0;
+  while (true) {
+    it[S - 1] = next();
+    if (it[S - 1] >= 0) {
+      R.release();
+      R.issue(tm, it[S - 1], wr);
+    }
+    if (it[0] < 0) break;
+    R.wait(rd);
+    body(it[0], R.slot(rd));
+    if (resident && lane == 0) resident[rd] = it[0];
+    ++n;
+#pragma unroll
+    for (int s = 0; s < S - 1; ++s) it[s] = it[s + 1];
+    rd = rd + 1 == S ? 0 : rd + 1;
+    wr = wr + 1 == S ? 0 : wr + 1;
+  }
+  return n;
+}
+
+template <int U, int S, int NW>
+__device__ __forceinline__ void init_mring(MRing<U, S>& R, int warp, int lane) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t bars[NW * S];
+  const uint32_t base = ((uint32_t)__cvta_generic_to_shared(smem_raw) + 1023u) & ~1023u;
+  R.init(base + (uint32_t)warp * S * MRing<U, S>::kItemBytes, (uint32_t)__cvta_generic_to_shared(&bars[warp * S]),
+         lane);
+}
+
+template <int U, int S, int NW>
+constexpr int mring_smem() { return NW * S * (int)MRing<U, S>::kItemBytes + 1024; }
+
+// MXFP4, single pass.  MB: CTAs per SM the register allocation must allow.
+template <int IN, int HK, int U, int S, int NW, int MB>
+__global__ void __launch_bounds__(NW * 32, MB)
+    k_act_quant_mx_mma(const __grid_constant__ CUtensorMap tmx, AQParams p) {
+  __shared__ uint32_t ctr;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  pdl_trigger();
+  const EncConsts k;
+  Trace tr(p, warp, lane);
+  if (threadIdx.x == 0) ctr = 0u;
+  MRing<U, S> R;
+  init_mring<U, S, NW>(R, warp, lane);
+  uint32_t hb[16], off[4];
+  hadamard_frags<IN, HK>(lane, hb);
+  ldsm_offsets(lane, off);
+  __syncthreads();
+  pdl_wait();
+  if (blockIdx.x == 0 && threadIdx.x == 0) *p.tensor_scale = k.st32;
+  CtaRange r;
+  r.init(p);
+  Claims cl;
+  cl.init(&ctr, r.cnt, lane);
+  uint32_t bad = 0;
+  const int n = run_ring(
+      &tmx, R, [&] { const int c = cl.next(lane); return c < 0 ? -1 : r.c0 + c; }, nullptr, lane,
+      [&](int item, uint32_t sbase) {
+#pragma unroll 1
+        for (int u = 0; u < U; ++u) {
+          u64 P[4][4];
+          rotate_tile<IN, HK>(sbase + u * 2048u, off, hb, lane, P);
+          encode_tile<MRFP4_FMT_MXFP4>(p, k, P, (uint32_t)(item * U + u) * 32u, lane, bad);
+        }
+      });
+  tr.end(n);
+  if (bad) atomic_or_status(p.status, bad);
+  zero_sf_padding(p);
+}
+
+// NVFP4: phase 1 (tensor max) -> grid barrier -> phase 2 (encode), as k_act_quant_nv.
+template <int IN, int HK, int U, int S, int NW, int MB>
+__global__ void __launch_bounds__(NW * 32, MB)
+    k_act_quant_nv_mma(const __grid_constant__ CUtensorMap tmx, AQParams p) {
+  __shared__ uint32_t ctr[2];
+  __shared__ int resident[NW][S];
+  __shared__ uint32_t marks[kBitmapWords];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t* ws = p.gmax;
+  volatile uint32_t* vgen = ws + 2;
+  const uint32_t gen0 = *vgen;
+  Trace tr(p, warp, lane);
+  CtaRange r;
+  r.init(p);
+  const bool use_marks = r.cnt <= 32 * kBitmapWords && p.marks != 0;
+  if (threadIdx.x < 2) ctr[threadIdx.x] = 0u;
+  if (lane < S) resident[warp][lane] = -1;
+  if (use_marks)
+    for (int i = threadIdx.x; i < (r.cnt + 31) / 32; i += NW * 32) marks[i] = 0u;
+  MRing<U, S> R;
+  init_mring<U, S, NW>(R, warp, lane);
+  uint32_t hb[16], off[4];
+  hadamard_frags<IN, HK>(lane, hb);
+  ldsm_offsets(lane, off);
+  __syncthreads();
+  pdl_wait();
+
+  float m = 0.f;
+  {
+    Claims cl;
+    cl.init(&ctr[0], r.cnt, lane);
+    run_ring(
+        &tmx, R, [&] { const int c = cl.next(lane); return c < 0 ? -1 : r.c0 + c; }, resident[warp], lane,
+        [&](int item, uint32_t sbase) {
+#pragma unroll 1
+          for (int u = 0; u < U; ++u) {
+            u64 P[4][4];
+            rotate_tile<IN, HK>(sbase + u * 2048u, off, hb, lane, P);
+            m = max3n(max3n(slot_amax(P[0]), slot_amax(P[1]), slot_amax(P[2])), slot_amax(P[3]), m);
+          }
+        });
+  }
+  __syncwarp();
+  tr.mark(3);
+  if (use_marks && lane < S) {
+    const int it = resident[warp][lane];
+    if (it >= 0) atomicOr(&marks[(it - r.c0) >> 5], 1u << ((it - r.c0) & 31));
+  }
+  uint32_t mb = __float_as_uint(m);
+  mb = mb > 0x7f800000u ? 0x7fc00000u : mb;
+  mb = __reduce_max_sync(0xffffffffu, mb);
+  __shared__ uint32_t smax[NW];
+  __shared__ EncConsts sk;
+  if (lane == 0) smax[warp] = mb;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t x = 0;
+    for (int i = 0; i < NW; ++i) x = max(x, smax[i]);
+    if (x) atomicMax(ws, x);
+    if (x >= 0x7f800000u) atomic_or_status(p.status, MRFP4_STATUS_NONFINITE);
+    __threadfence();
+    if (atomicAdd(ws + 1, 1u) == gridDim.x - 1) {
+      ws[1] = 0u;
+      __threadfence();
+      atomicAdd(ws + 2, 1u);
+    } else {
+      uint32_t g;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(ws + 2) : "memory");
+      } while (g == gen0);
+    }
+    __threadfence();
+    sk = nv_consts(p, *(volatile uint32_t*)ws);
+  }
+  __syncthreads();
+  tr.mark(4);
+  pdl_trigger();
+  const EncConsts k = sk;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *p.tensor_scale = k.st32;
+
+  uint32_t bad = 0;
+  auto encode = [&](int item, uint32_t sbase) {
+#pragma unroll 1
+    for (int u = 0; u < U; ++u) {
+      u64 P[4][4];
+      rotate_tile<IN, HK>(sbase + u * 2048u, off, hb, lane, P);
+      encode_tile<MRFP4_FMT_NVFP4>(p, k, P, (uint32_t)(item * U + u) * 32u, lane, bad);
+    }
+  };
+  if (use_marks) {
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      const int it = resident[warp][s];
+      if (it >= 0) encode(it, R.slot(s));
+    }
+  }
+  Claims cl;
+  cl.init(&ctr[1], r.cnt, lane);
+  const int n = run_ring(
+      &tmx, R,
+      [&] {
+        while (true) {
+          const int c = cl.next(lane);
+          if (c < 0) return -1;
+          const int o = r.cnt - 1 - c;
+          if (!use_marks || !((marks[o >> 5] >> (o & 31)) & 1u)) return r.c0 + o;
+        }
+      },
+      nullptr, lane, encode);
+  tr.end(n);
+  if (bad) atomic_or_status(p.status, bad);
+  zero_sf_padding(p);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(ws + 3, 1u) == gridDim.x - 1) {
+      ws[0] = 0u;
+      ws[3] = 0u;
+      __threadfence();
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // QuantResult metrics (quantizers.py:218-231): mse_rel = sum (y - q)^2 / sum y^2 and
 // mse_top_rel = mean over groups of ((y_top - q_top) / y_top)^2 at each group's argmax |y|
 // (first index on ties, like np.argmax), all in the rotated domain.  Sums in fp64 with
@@ -1084,13 +1621,13 @@ int launch_persistent(int smem, const CUtensorMap& tm, const AQParams& p, cudaSt
 // FlatWalk's TMA view of X: [total_segs rows][one segment = kLaneBytes] bytes, box = one
 // item (32 segments), swizzled like the cp.async ring (64 B rows: SWIZZLE_64B, 128 B: 128B).
 template <int IN>
-bool make_segment_map(CUtensorMap* tm, const AQParams& p) {
+bool make_segment_map(CUtensorMap* tm, const AQParams& p, int box_segs = 32) {
   using C = InCfg<IN>;
   auto encode = tensor_map_encoder();
   if (!encode) return false;
   cuuint64_t dims[2] = {(cuuint64_t)C::kLaneBytes, (cuuint64_t)p.total_segs};
   cuuint64_t strides[1] = {(cuuint64_t)C::kLaneBytes};
-  cuuint32_t box[2] = {(cuuint32_t)C::kLaneBytes, 32};
+  cuuint32_t box[2] = {(cuuint32_t)C::kLaneBytes, (cuuint32_t)box_segs};
   cuuint32_t estr[2] = {1, 1};
   return encode(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(p.x), dims, strides, box, estr,
                 CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -1109,8 +1646,36 @@ int launch_nw(const AQParams& p, const CUtensorMap& tm, cudaStream_t s) {
   return launch_persistent<k_act_quant_mx<IN, HK, GenWalk, NW>, NW>(smem, tm, p, s);
 }
 
+// K1m launch: U tiles per item, S ring stages, NW warps per CTA.
+template <int IN, int FMT, int HK, int U, int S, int NW, int MB>
+int launch_mma_cfg(AQParams p, cudaStream_t s) {
+  CUtensorMap tm;
+  memset(&tm, 0, sizeof(tm));
+  if (!make_segment_map<IN>(&tm, p, 32 * U)) return MRFP4_ECUDA;
+  p.items = ceil_div((int64_t)p.total_segs, 32 * U);
+  constexpr int smem = mring_smem<U, S, NW>();
+  if constexpr (FMT == MRFP4_FMT_NVFP4)
+    return launch_persistent<k_act_quant_nv_mma<IN, HK, U, S, NW, MB>, NW>(smem, tm, p, s);
+  return launch_persistent<k_act_quant_mx_mma<IN, HK, U, S, NW, MB>, NW>(smem, tm, p, s);
+}
+
+// Two tiles per item (fewer claims / TMA issues per tile) once every warp gets >= 8 tiles;
+// one tile per item below that (more items to balance over the SM's warps).  Capping the
+// registers for a third 8-warp CTA per SM spills and measured 1.4-1.6x slower.
+template <int IN, int FMT, int HK>
+int launch_mma(const AQParams& p, cudaStream_t s) {
+  const int64_t tiles = ceil_div((int64_t)p.total_segs, 32);
+  int cfg = knob("MRFP4_K1M_CFG", -1);
+  if (cfg < 0) cfg = tiles >= 8 * 16 * (int64_t)num_sms() ? 1 : 0;
+  return cfg == 0 ? launch_mma_cfg<IN, FMT, HK, 1, 3, 8, 1>(p, s) : launch_mma_cfg<IN, FMT, HK, 2, 3, 8, 1>(p, s);
+}
+
 template <int IN, int FMT, int HK>
 int launch_hk(const AQParams& p, cudaStream_t s) {
+  if constexpr (IN != MRFP4_DT_F32 && HK >= 16) {
+    // Tensor-core rotation: contiguous bf16 / f16 rows with K % 32 == 0, K >= 1024.
+    if (p.nseg && knob("MRFP4_K1_MMA", 1)) return launch_mma<IN, FMT, HK>(p, s);
+  }
   CUtensorMap tm;
   memset(&tm, 0, sizeof(tm));
   if (p.nseg && !make_segment_map<IN>(&tm, p)) return MRFP4_ECUDA;

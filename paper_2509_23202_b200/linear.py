@@ -14,6 +14,7 @@ gptq.py:274-300).  Here:
 * ``quantize_weight`` is the GPU RTN of a dense weight (bit-identical to
   ``quantize_rtn(W, spec, transform=H_k)``, transforms.py:94-100 rotation folded).
 * ``quantized_linear`` runs K1 on the activations and K2 (tcgen05 block-scaled GEMM).
+* ``quantized_linear_host`` is the same on host buffers, copies pipelined with compute.
 """
 
 from __future__ import annotations
@@ -26,7 +27,7 @@ import torch
 
 from . import _lib
 from .errors import DataError
-from .formats import GROUP, format_code, spec_for
+from .formats import FMT_NVFP4 as FMT_NVFP4_CODE, GROUP, format_code, spec_for
 from .quantize import GpuQuantResult, act_quant_into, alloc_result, as_device_matrix, quantize_rtn
 from .transforms import hadamard_block, transform_for
 
@@ -178,3 +179,98 @@ def quantized_linear(x, w: PackedWeight, *, out_dtype=torch.bfloat16, out: torch
         out = torch.empty((M, w.N), dtype=out_dtype, device=x2.device)
     gemm(a, w, out)
     return out.reshape(*lead, w.N) if lead is not None and len(lead) != 1 else out
+
+
+class _HostPipe:
+    """Per-(device, weight shape, chunk) device buffers and streams of quantized_linear_host."""
+
+    def __init__(self, device, rows: int, K: int, N: int, fmt: int, had_k: int, x_dtype, out_dtype):
+        self.x = [torch.empty((rows, K), dtype=x_dtype, device=device) for _ in range(2)]
+        self.a = [alloc_result(rows, K, fmt, had_k, device) for _ in range(2)]
+        self.y = [torch.empty((rows, N), dtype=out_dtype, device=device) for _ in range(2)]
+        self.s_in = torch.cuda.Stream(device)
+        self.s_comp = torch.cuda.Stream(device)
+        self.s_out = torch.cuda.Stream(device)
+
+
+_PIPES: dict = {}
+
+
+def quantized_linear_host(x: torch.Tensor, w: PackedWeight, *, out: torch.Tensor | None = None,
+                          out_dtype=torch.bfloat16, chunk_rows: int | None = None) -> torch.Tensor:
+    """``quantized_linear`` on HOST buffers (the reference's CPU arrays in, arrays out).
+
+    x is a CPU tensor [M, K] (bf16 / fp16 / fp32; pinned for asynchronous copies), the result
+    is a CPU tensor [M, N] (``out`` if given, pinned).  Returns once the work is queued; the
+    caller's current stream is ordered after the last device->host copy (synchronize it, or
+    an event on it, before reading ``out``).
+
+    MXFP4 scales are group-local, so rows are processed in chunks on three streams: the
+    host->device copy of chunk i+1, K1+K2 of chunk i and the device->host copy of chunk i-1
+    overlap (PCIe is full duplex), and the result is identical to one whole-matrix call.
+    NVFP4's tensor scale is a max over the WHOLE activation (quantizers.py:198-200), so no
+    row of it can be encoded before every row has arrived: NVFP4 runs copy -> K1+K2 -> copy.
+    """
+    if not isinstance(w, PackedWeight):
+        w = prepare_weight(w)
+    if x.device.type != "cpu" or x.dim() != 2:
+        raise DataError("quantized_linear_host expects a 2-D CPU tensor")
+    if out_dtype not in _OUT:
+        raise DataError("out_dtype must be torch.bfloat16 or torch.float32")
+    M, K = x.shape
+    if K != w.K:
+        raise DataError(f"activation K={K} does not match weight K={w.K}")
+    if x.dtype not in (torch.bfloat16, torch.float16, torch.float32):
+        x = x.float()
+    x = x.contiguous()
+    if not x.is_pinned():
+        x = x.pin_memory()
+    if out is None:
+        out = torch.empty((M, w.N), dtype=out_dtype, pin_memory=True)
+    elif out.shape != (M, w.N) or out.dtype not in _OUT or out.device.type != "cpu":
+        raise DataError("out must be a CPU tensor [M, N] of bf16 / fp32")
+    dev = w.device
+    cur = torch.cuda.current_stream(dev)
+    if w.fmt == FMT_NVFP4_CODE or M <= 128:
+        xd = x.to(dev, non_blocking=True)
+        y = quantized_linear(xd, w, out_dtype=out.dtype)
+        out.copy_(y, non_blocking=True)
+        return out
+    rows = chunk_rows or max(128, ((M + 7) // 8 + 127) // 128 * 128)   # ~8 chunks
+    key = (dev, rows, K, w.N, w.fmt, w.had_k, x.dtype, out.dtype)
+    pipe = _PIPES.get(key)
+    if pipe is None:
+        pipe = _PIPES[key] = _HostPipe(dev, rows, K, w.N, w.fmt, w.had_k, x.dtype, out.dtype)
+    start = torch.cuda.Event()
+    start.record(cur)
+    ev_in, ev_comp, ev_out = {}, {}, {}
+    for i, r0 in enumerate(range(0, M, rows)):
+        r1 = min(M, r0 + rows)
+        n = r1 - r0
+        b = i & 1
+        with torch.cuda.stream(pipe.s_in):
+            pipe.s_in.wait_event(start)
+            if i >= 2:
+                pipe.s_in.wait_event(ev_comp[i - 2])       # K1 of chunk i-2 has read x[b]
+            pipe.x[b][:n].copy_(x[r0:r1], non_blocking=True)
+            ev_in[i] = torch.cuda.Event()
+            ev_in[i].record(pipe.s_in)
+        with torch.cuda.stream(pipe.s_comp):
+            pipe.s_comp.wait_event(ev_in[i])
+            if i >= 2:
+                pipe.s_comp.wait_event(ev_out[i - 2])      # y[b] of chunk i-2 copied out
+            a = pipe.a[b]
+            if n != rows:
+                a = alloc_result(n, K, w.fmt, w.had_k, dev)
+            act_quant_into(pipe.x[b][:n], w.fmt, w.had_k, a.codes, a.sf, a.tensor_scale_dev, a.scratch)
+            gemm(a, w, pipe.y[b][:n])
+            ev_comp[i] = torch.cuda.Event()
+            ev_comp[i].record(pipe.s_comp)
+        with torch.cuda.stream(pipe.s_out):
+            pipe.s_out.wait_event(ev_comp[i])
+            out[r0:r1].copy_(pipe.y[b][:n], non_blocking=True)
+            ev_out[i] = torch.cuda.Event()
+            ev_out[i].record(pipe.s_out)
+    cur.wait_event(ev_out[max(ev_out)])
+    cur.wait_event(ev_comp[max(ev_comp)])
+    return out

@@ -238,3 +238,40 @@ def test_metrics_against_golden(golden):
         assert gpu.mse_top_rel == pytest.approx(float(golden[key + "_msetop"]), rel=1e-6), key
         n += 1
     assert n > 0
+
+
+@pytest.mark.parametrize("fmt", ["mxfp4", "nvfp4"])
+@pytest.mark.parametrize("k", [16, 32, 64, 128])
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+def test_tensor_core_rotation_matches_butterfly(monkeypatch, fmt, k, dtype):
+    """K1m (Hadamard on the tensor cores, quad-distributed scales) vs K1 (fp32 butterfly):
+    both are exact whenever a block's sum fits fp32, so codes agree except where an inexact
+    sum lands within an ulp of a rounding boundary; both stay within the oracle bar."""
+    rng = np.random.default_rng(zlib.crc32(f"mma{fmt}{k}{dtype}".encode()))
+    M, K = 333, 4096 + 1024   # partial last tile of the flat walk
+    X = rng.standard_normal((M, K)) * np.exp2(rng.integers(-6, 7, (M, 1)))
+    X = X.astype(np.float16).astype(np.float64) if dtype == torch.float16 else O.bf16_round(X)
+    ora = O.quantize_rtn(X, fmt, hadamard=k)
+    outs = {}
+    for mma in ("1", "0"):
+        monkeypatch.setenv("MRFP4_K1_MMA", mma)
+        g = P.quantize_rtn(_gpu(X, dtype), SPEC[fmt], transform=_tr(k))
+        outs[mma] = _host(g)
+        code_rate, scale_rate, _ = _match(g, ora)
+        assert code_rate >= 0.9999 and scale_rate >= 0.9999, (mma, code_rate, scale_rate)
+    (c1, s1, t1), (c0, s0, t0) = outs["1"], outs["0"]
+    assert (c1 == c0).mean() >= 0.99999 and (s1 == s0).mean() >= 0.99999
+    assert t1 == pytest.approx(t0, rel=2 ** -22)
+
+
+@pytest.mark.parametrize("cfg", ["0", "1"])
+@pytest.mark.parametrize("fmt,k", [("mxfp4", 32), ("nvfp4", 16), ("nvfp4", 128)])
+def test_tensor_core_rotation_configs_identical(monkeypatch, cfg, fmt, k):
+    """Every K1m work split (tiles per item, ring depth) produces identical bytes."""
+    rng = np.random.default_rng(3)
+    X = torch.from_numpy(O.bf16_round(rng.standard_normal((777, 3072)))).cuda().bfloat16()
+    monkeypatch.setenv("MRFP4_K1M_CFG", "1")
+    ref = _host(P.quantize_rtn(X, SPEC[fmt], transform=_tr(k)))
+    monkeypatch.setenv("MRFP4_K1M_CFG", cfg)
+    got = _host(P.quantize_rtn(X, SPEC[fmt], transform=_tr(k)))
+    assert np.array_equal(ref[0], got[0]) and np.array_equal(ref[1], got[1]) and ref[2] == got[2]

@@ -176,3 +176,22 @@ def test_weight_validation():
     q2 = random_container(rng, 128, 96, "mxfp4")
     with pytest.raises(P.DataError, match="multiple of 64"):
         P.prepare_weight(to_mfp(q2))
+
+
+@pytest.mark.parametrize("fmt,k,M", [("mxfp4", 32, 2048), ("mxfp4", 128, 1000), ("nvfp4", 16, 700), ("mxfp4", 32, 100)])
+def test_host_pipeline_matches_device_call(fmt, k, M):
+    """quantized_linear_host (row chunks over three streams for MXFP4) == quantized_linear."""
+    rng = np.random.default_rng(M + k)
+    K, N = 2048, 768
+    X = torch.from_numpy(O.bf16_round(rng.standard_normal((M, K)))).bfloat16()
+    W = torch.from_numpy(O.bf16_round(rng.standard_normal((N, K)) / 45)).bfloat16().cuda()
+    w = P.quantize_weight(W, SPEC[fmt], P.TransformSpec.hadamard(k))
+    ref = P.quantized_linear(X.cuda(), w).cpu()
+    for chunk in (None, 256, 384):
+        y = P.quantized_linear_host(X.pin_memory(), w, chunk_rows=chunk)
+        torch.cuda.synchronize()
+        assert y.device.type == "cpu" and torch.equal(y, ref), chunk
+    out = torch.empty((M, N), dtype=torch.float32).pin_memory()
+    P.quantized_linear_host(X, w, out=out)
+    torch.cuda.synchronize()
+    assert torch.equal(out, P.quantized_linear(X.cuda(), w, out_dtype=torch.float32).cpu())
