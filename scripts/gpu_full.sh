@@ -1,5 +1,6 @@
 #!/bin/bash
-# One GPU-box evidence pass: tests, smoke, bench (all configs), ncu launch list + full captures.
+# One GPU-box evidence pass: tests, smoke, bench (all configs + reference arm + 70B token sweep),
+# ncu launch list + full captures of K1 and K2 (reports reduced to CSV; .ncu-rep removed).
 set -x
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/gpu.txt 2>&1
@@ -10,14 +11,16 @@ for c in c0 c2-up-nv c2-down-mx c3-gateup; do
   timeout 300 python bench.py --config $c --steps 200 --no-cpu-baseline > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err
 done
 timeout 300 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
+rm -f gpurun_out/sweep.jsonl; timeout 900 bash scripts/sweep.sh > gpurun_out/sweep.txt 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 60 --csv \
   --log-file gpurun_out/launches_c1.csv python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_launch.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_gemm -s 3 -c 1 -f -o gpurun_out/prof_gemm_c1 \
-  python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_gemm.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_act_quant -s 3 -c 1 -f -o gpurun_out/prof_k1_c1 \
-  python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_k1.log 2>&1
-for f in prof_gemm_c1 prof_k1_c1; do
-  ncu -i gpurun_out/$f.ncu-rep --page details --csv > gpurun_out/${f}_details.csv 2>/dev/null
-  ncu -i gpurun_out/$f.ncu-rep --page raw --csv > gpurun_out/${f}_raw.csv 2>/dev/null
+for cfg in c1 c2-up-nv; do
+  for kk in k_gemm k_act_quant; do
+    timeout 900 ncu --set full --clock-control none --import-source on -k regex:$kk -s 3 -c 1 -f -o gpurun_out/prof_${kk}_$cfg \
+      python bench.py --config $cfg --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_${kk}_$cfg.log 2>&1
+    ncu -i gpurun_out/prof_${kk}_$cfg.ncu-rep --page details --csv > gpurun_out/prof_${kk}_${cfg}_details.csv 2>/dev/null
+    ncu -i gpurun_out/prof_${kk}_$cfg.ncu-rep --page raw --csv > gpurun_out/prof_${kk}_${cfg}_raw.csv 2>/dev/null
+    rm -f gpurun_out/prof_${kk}_$cfg.ncu-rep
+  done
 done
 ls -la gpurun_out
