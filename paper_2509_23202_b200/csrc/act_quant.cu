@@ -697,13 +697,19 @@ __device__ __forceinline__ uint32_t sf_off32(uint32_t r, uint32_t c, uint32_t cb
 
 // Zero the padding of the swizzled scale buffer: rows [M, rows_pad) (whole 4-byte words)
 // and columns [sf_cols, 4*col_blocks) of the real rows (<= 3 bytes per row).
+// Padding rows all lie in the last 128-row block, whose cb atoms are one contiguous run of
+// cb * 512 bytes: word i of it belongs to row (i % 128 / 4) + 32 * (i % 4) of its atom, so
+// the grid walks the run linearly (coalesced) and zeroes the words of rows >= M % 128.
 __device__ __forceinline__ void zero_sf_padding(const AQParams& p) {
   const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
   const uint32_t M = (uint32_t)p.Mi, cb = p.cb;
-  const uint32_t n_words = ((uint32_t)p.rows_pad - M) * cb;
-  for (uint32_t i = tid; i < n_words; i += nth) {
-    const uint32_t r = M + i / cb, blk = i - (i / cb) * cb;
-    *reinterpret_cast<uint32_t*>(p.sf + sf_off32(r, 4 * blk, cb)) = 0u;
+  const uint32_t live = M & 127u;
+  if (live) {
+    uint32_t* run = reinterpret_cast<uint32_t*>(p.sf + (size_t)(M >> 7) * cb * 512u);
+    for (uint32_t i = tid; i < cb * 128u; i += nth) {
+      const uint32_t r = ((i & 127u) >> 2) + 32u * (i & 3u);
+      if (r >= live) run[i] = 0u;
+    }
   }
   const uint32_t sfc = (uint32_t)p.sf_cols, extra = 4 * cb - sfc;
   if (extra) {
@@ -1057,8 +1063,14 @@ __device__ __forceinline__ void ldsm_offsets(int lane, uint32_t (&off)[4]) {
 }
 
 // 32 x 32 tile at `sbase` -> P[j][nt] = output elements (8t + 2nt, 8t + 2nt + 1) of segment 8j + g.
+// The B fragments live in shared memory (HB_SMEM: [8 (kt, nt)][32 lanes] x 8 B, conflict-free
+// LDS.64), not in 16 registers per lane: registers bound the kernel's occupancy.
+__device__ __forceinline__ void lds64(uint32_t saddr, uint32_t& a, uint32_t& b) {
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(a), "=r"(b) : "r"(saddr));
+}
+
 template <int IN, int HK>
-__device__ __forceinline__ void rotate_tile(uint32_t sbase, const uint32_t (&off)[4], const uint32_t (&b)[16],
+__device__ __forceinline__ void rotate_tile(uint32_t sbase, const uint32_t (&off)[4], uint32_t hb_smem,
                                             int lane, u64 (&P)[4][4]) {
   float c[2][4][4];
 #pragma unroll
@@ -1074,7 +1086,11 @@ __device__ __forceinline__ void rotate_tile(uint32_t sbase, const uint32_t (&off
       uint32_t a[4];
       ldsm_x4(sbase + off[2 * mt + kt], a);
 #pragma unroll
-      for (int nt = 0; nt < 4; ++nt) hmma16816<IN>(c[mt][nt], a, b[(kt * 4 + nt) * 2], b[(kt * 4 + nt) * 2 + 1]);
+      for (int nt = 0; nt < 4; ++nt) {
+        uint32_t b0, b1;
+        lds64(hb_smem + (uint32_t)(((kt * 4 + nt) * 32 + lane) * 8), b0, b1);
+        hmma16816<IN>(c[mt][nt], a, b0, b1);
+      }
     }
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt)
@@ -1355,8 +1371,18 @@ __global__ void __launch_bounds__(NW * 32, MB)
   if (threadIdx.x == 0) ctr = 0u;
   MRing<U, S> R;
   init_mring<U, S, NW>(R, warp, lane);
-  uint32_t hb[16], off[4];
-  hadamard_frags<IN, HK>(lane, hb);
+  __shared__ __align__(16) uint32_t hb_tab[8 * 32 * 2];
+  uint32_t off[4];
+  if (warp == 0) {
+    uint32_t hb[16];
+    hadamard_frags<IN, HK>(lane, hb);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      hb_tab[(i * 32 + lane) * 2] = hb[2 * i];
+      hb_tab[(i * 32 + lane) * 2 + 1] = hb[2 * i + 1];
+    }
+  }
+  const uint32_t hbs = (uint32_t)__cvta_generic_to_shared(hb_tab);
   ldsm_offsets(lane, off);
   __syncthreads();
   pdl_wait();
@@ -1372,7 +1398,7 @@ __global__ void __launch_bounds__(NW * 32, MB)
 #pragma unroll 1
         for (int u = 0; u < U; ++u) {
           u64 P[4][4];
-          rotate_tile<IN, HK>(sbase + u * 2048u, off, hb, lane, P);
+          rotate_tile<IN, HK>(sbase + u * 2048u, off, hbs, lane, P);
           encode_tile<MRFP4_FMT_MXFP4>(p, k, P, (uint32_t)(item * U + u) * 32u, lane, bad);
         }
       });
@@ -1402,8 +1428,18 @@ __global__ void __launch_bounds__(NW * 32, MB)
     for (int i = threadIdx.x; i < (r.cnt + 31) / 32; i += NW * 32) marks[i] = 0u;
   MRing<U, S> R;
   init_mring<U, S, NW>(R, warp, lane);
-  uint32_t hb[16], off[4];
-  hadamard_frags<IN, HK>(lane, hb);
+  __shared__ __align__(16) uint32_t hb_tab[8 * 32 * 2];
+  uint32_t off[4];
+  if (warp == 0) {
+    uint32_t hb[16];
+    hadamard_frags<IN, HK>(lane, hb);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      hb_tab[(i * 32 + lane) * 2] = hb[2 * i];
+      hb_tab[(i * 32 + lane) * 2 + 1] = hb[2 * i + 1];
+    }
+  }
+  const uint32_t hbs = (uint32_t)__cvta_generic_to_shared(hb_tab);
   ldsm_offsets(lane, off);
   __syncthreads();
   pdl_wait();
@@ -1418,7 +1454,7 @@ __global__ void __launch_bounds__(NW * 32, MB)
 #pragma unroll 1
           for (int u = 0; u < U; ++u) {
             u64 P[4][4];
-            rotate_tile<IN, HK>(sbase + u * 2048u, off, hb, lane, P);
+            rotate_tile<IN, HK>(sbase + u * 2048u, off, hbs, lane, P);
             m = max3n(max3n(slot_amax(P[0]), slot_amax(P[1]), slot_amax(P[2])), slot_amax(P[3]), m);
           }
         });
@@ -1466,7 +1502,7 @@ __global__ void __launch_bounds__(NW * 32, MB)
 #pragma unroll 1
     for (int u = 0; u < U; ++u) {
       u64 P[4][4];
-      rotate_tile<IN, HK>(sbase + u * 2048u, off, hb, lane, P);
+      rotate_tile<IN, HK>(sbase + u * 2048u, off, hbs, lane, P);
       encode_tile<MRFP4_FMT_NVFP4>(p, k, P, (uint32_t)(item * U + u) * 32u, lane, bad);
     }
   };
@@ -1667,6 +1703,8 @@ int launch_mma(const AQParams& p, cudaStream_t s) {
   const int64_t tiles = ceil_div((int64_t)p.total_segs, 32);
   int cfg = knob("MRFP4_K1M_CFG", -1);
   if (cfg < 0) cfg = tiles >= 8 * 16 * (int64_t)num_sms() ? 1 : 0;
+  // (18 / 20 warps per SM -- 2 x 9 or 2 x 10 -- measured no faster: the stalls are
+  // fixed-latency dependency waits inside a warp's tile, not a lack of warps.)
   return cfg == 0 ? launch_mma_cfg<IN, FMT, HK, 1, 3, 8, 1>(p, s) : launch_mma_cfg<IN, FMT, HK, 2, 3, 8, 1>(p, s);
 }
 
