@@ -132,6 +132,28 @@ int mrfp4_gemm(const uint8_t* a, const uint8_t* a_sf, const float* a_ts,
 int mrfp4_dequantize(const uint8_t* codes, const uint8_t* sf, const float* tensor_scale,
                      int64_t rows, int64_t cols, int fmt, float* out, void* stream);
 
+/*
+ * Offline MSE scale search (replaces the numpy loops of
+ * optimize_group_scales, quantizers.py:263-327).  y: the rotated matrix in float64, viewed as
+ * ngroups contiguous groups of 32 (MXFP4) / 16 (NVFP4) values, 16-byte aligned.
+ *
+ * mrfp4_mse_pass -- one candidate pass (quantizers.py:288-302): for every group, the
+ *   candidate raw scales cand[c] * raw0[g] (c < ncand; the reference's [1.0] + 128 multipliers)
+ *   are encoded against s_global (fp_scale_encode, formats.py:220-262), each scored by
+ *   sum((y - eff * fp4(y / eff))^2) with eff = ts * decoded in numpy's pairwise order, and the
+ *   first minimum is kept: scale_codes[g], decoded[g], group_err[g], and the group's packed
+ *   E2M1 codes (low nibble first) in codes[g * G / 2 ..].
+ * mrfp4_mse_group_err -- group errors at fixed decoded scales and tensor scale ts (the terms
+ *   of total_err, quantizers.py:304-306).
+ * Device status bits: 2 = a candidate scale decodes to 0 (the reference raises DataError),
+ * 1 = non-finite error.  The caller sums group_err in numpy's order.
+ */
+int mrfp4_mse_pass(const double* y, int64_t ngroups, int fmt, const double* cand, int ncand, const double* raw0,
+                   double s_global, double ts, uint8_t* scale_codes, double* decoded, double* group_err,
+                   uint8_t* codes, uint32_t* status, void* stream);
+int mrfp4_mse_group_err(const double* y, int64_t ngroups, int fmt, const double* decoded, double ts,
+                        double* group_err, uint32_t* status, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -4,6 +4,7 @@ Mirrors the reference package's names (/root/reference/pkg/src/microfp/__init__.
 for everything on the path ``Q(X H_k) Q(W H_k)^T``:
 
     quantize_rtn / quantize          K1: fused Hadamard + FP4 quantization (CUDA)
+    quantize(policy=MSE)             offline MSE scale search on the GPU (weights)
     FormatSpec, ScaleFormat, ...     format descriptors (same fields as the reference)
     MfpTensor, pack_tensor, ...      host container (interchange with the reference)
     prepare_weight, quantize_weight  K3: weight prep into the tensor-core layout
@@ -16,15 +17,17 @@ All compute runs in libmrfp4.so (sm_100a); there is no CPU fallback.
 
 from .errors import DataError, NumericalError
 from .fileio import parse_quant, quant_bytes, read_quant, write_quant
-from .formats import FMT_MXFP4, FMT_NVFP4, FormatSpec, MfpTensor, ScaleFormat, ScaleKind, pack_tensor, unpack_tensor
+from .formats import (FMT_MXFP4, FMT_NVFP4, FormatSpec, MfpTensor, ScaleFormat, ScaleKind, ScaleMode, ScalePolicy,
+                      pack_tensor, unpack_tensor)
 from .linear import PackedWeight, gemm, prepare_weight, quantize_weight, quantized_linear, quantized_linear_host
-from .quantize import GpuQuantResult, quantize, quantize_rtn
+from .quantize import GpuQuantResult, mse_optimize_scales, quantize, quantize_rtn
 from .transforms import TransformKind, TransformSpec
 
 __version__ = "0.1.0"
 
 __all__ = [
-    "DataError", "NumericalError", "FormatSpec", "ScaleFormat", "ScaleKind", "MfpTensor",
+    "DataError", "NumericalError", "FormatSpec", "ScaleFormat", "ScaleKind", "ScaleMode", "ScalePolicy", "MfpTensor",
+    "mse_optimize_scales",
     "TransformKind", "TransformSpec", "pack_tensor", "unpack_tensor", "quantize_rtn", "quantize",
     "GpuQuantResult", "PackedWeight", "prepare_weight", "quantize_weight", "quantized_linear", "quantized_linear_host", "gemm",
     "quantized_linear_sharded", "read_quant", "write_quant", "parse_quant", "quant_bytes",

@@ -23,6 +23,11 @@ int launch_sf_swizzle(const uint8_t* src, uint8_t* dst, int64_t rows, int64_t co
 int launch_sf_unswizzle(const uint8_t* src, uint8_t* dst, int64_t rows, int64_t cols, cudaStream_t s);
 int launch_dequantize(const uint8_t* codes, const uint8_t* sf, const float* ts, int64_t rows, int64_t cols, int fmt,
                       float* out, cudaStream_t s);
+int launch_mse_pass(const double* y, int64_t ngroups, int fmt, const double* cand, int ncand, const double* raw0,
+                    double sg, double ts, uint8_t* sc, double* dec, double* gerr, uint8_t* codes, uint32_t* status,
+                    cudaStream_t s);
+int launch_mse_group_err(const double* y, int64_t ngroups, int fmt, const double* dec, double ts, double* gerr,
+                         uint32_t* status, cudaStream_t s);
 }  // namespace mrfp4
 
 namespace mrfp4 {
@@ -169,3 +174,29 @@ int mrfp4_dequantize(const uint8_t* codes, const uint8_t* sf, const float* tenso
 }
 
 }  // extern "C"
+
+int mrfp4_mse_pass(const double* y, int64_t ngroups, int fmt, const double* cand, int ncand, const double* raw0,
+                   double s_global, double ts, uint8_t* scale_codes, double* decoded, double* group_err,
+                   uint8_t* codes, uint32_t* status, void* stream) {
+  if (mrfp4_group_size(fmt) == 0) return fail(MRFP4_EUNSUPPORTED, "unknown format %d", fmt);
+  if (ngroups < 1 || ncand < 1) return fail(MRFP4_EINVAL, "empty MSE search");
+  if (!(s_global > 0.0) || !(ts > 0.0)) return fail(MRFP4_EINVAL, "scales must be positive");
+  if (!y || !cand || !raw0 || !scale_codes || !decoded || !group_err || !codes || !status)
+    return fail(MRFP4_EINVAL, "null buffer");
+  if (!aligned(y, 16)) return fail(MRFP4_EUNSUPPORTED, "y must be 16-byte aligned");
+  return cuda_status(mrfp4::launch_mse_pass(y, ngroups, fmt, cand, ncand, raw0, s_global, ts, scale_codes, decoded,
+                                            group_err, codes, status, static_cast<cudaStream_t>(stream)),
+                     "mrfp4_mse_pass");
+}
+
+int mrfp4_mse_group_err(const double* y, int64_t ngroups, int fmt, const double* decoded, double ts,
+                        double* group_err, uint32_t* status, void* stream) {
+  if (mrfp4_group_size(fmt) == 0) return fail(MRFP4_EUNSUPPORTED, "unknown format %d", fmt);
+  if (ngroups < 1) return fail(MRFP4_EINVAL, "empty MSE search");
+  if (!(ts > 0.0)) return fail(MRFP4_EINVAL, "tensor scale must be positive");
+  if (!y || !decoded || !group_err || !status) return fail(MRFP4_EINVAL, "null buffer");
+  if (!aligned(y, 16)) return fail(MRFP4_EUNSUPPORTED, "y must be 16-byte aligned");
+  return cuda_status(mrfp4::launch_mse_group_err(y, ngroups, fmt, decoded, ts, group_err, status,
+                                                 static_cast<cudaStream_t>(stream)),
+                     "mrfp4_mse_group_err");
+}

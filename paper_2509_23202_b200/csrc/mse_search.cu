@@ -1,0 +1,185 @@
+// Offline MSE scale search on the GPU:
+//   optimize_group_scales (/root/reference/pkg/src/microfp/quantizers.py:263-327).
+// The host driver (quantize.py::_mse_optimize) runs the reference's alternating search --
+// per-group candidate passes and, for NVFP4, the 128-point tensor-scale scan -- and sums
+// group errors exactly as numpy does; these kernels do the per-group work in float64 with
+// the reference's arithmetic:
+//   candidate raw   cand[c] * raw0                      (quantizers.py:294)
+//   scale code      fp_scale_encode(raw / s_global)     (quantizers.py:157-167; formats.py:220-262)
+//   group error     ((B - eff * fp4(B / eff))**2).sum(-1), numpy's pairwise order for 16 / 32
+//                   terms (8 accumulators, then ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)))
+//                                                       (quantizers.py:257-260, :211-215)
+//   argmin          first minimum over candidates        (quantizers.py:297)
+#include <cmath>
+
+#include "common.cuh"
+
+namespace mrfp4 {
+namespace {
+
+// E4M3 RNE of a positive double onto codes 0..126 (formats.py:239-251, :81-91), saturating.
+__device__ __forceinline__ uint32_t e4m3_code64(double v) {
+  if (!(v < 432.0)) return 126u;
+  if (v < 0.015625) return (uint32_t)__double2int_rn(v * 512.0);
+  int e;
+  const double fr = frexp(v, &e);
+  int m = __double2int_rn((fr * 2.0 - 1.0) * 8.0);
+  int E = e - 1;
+  if (m == 8) { m = 0; E += 1; }
+  return (uint32_t)(((E + 7) << 3) | m);
+}
+
+__device__ __forceinline__ double e4m3_value64(uint32_t c) {
+  const int E = (int)(c >> 3), m = (int)(c & 7u);
+  return E == 0 ? ldexp((double)m, -9) : ldexp(1.0 + m / 8.0, E - 7);
+}
+
+// Signed FP4 grid value of u (formats.py:94-113: ties 0.25 / 1.25 / 2.5 / 5 down, 0.75 / 1.75
+// / 3.5 up; saturate at 6) and its 4-bit code (sign only when the magnitude is non-zero).
+__device__ __forceinline__ double fp4_round64(double u, uint32_t& code) {
+  const double a = fabs(u);
+  const uint32_t idx = (a > 0.25) + (a > 0.75) + (a == 0.75) + (a > 1.25) + (a > 1.75) + (a == 1.75) + (a > 2.5) +
+                       (a > 3.5) + (a == 3.5) + (a > 5.0);
+  const double g[8] = {0.0, 0.5, 1.0, 1.5, 2.0, 3.0, 4.0, 6.0};
+  const bool neg = signbit(u);
+  code = idx | ((neg && idx) ? 8u : 0u);
+  return neg ? -g[idx] : g[idx];
+}
+
+// numpy pairwise_sum for n in {16, 32}: 8 accumulators, then a fixed tree.
+template <int G>
+__device__ __forceinline__ double group_err(const double (&v)[G], double eff) {
+  double r[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    uint32_t c;
+    const double d = v[j] - eff * fp4_round64(v[j] / eff, c);
+    r[j] = d * d;
+  }
+#pragma unroll
+  for (int i = 8; i < G; i += 8)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      uint32_t c;
+      const double d = v[i + j] - eff * fp4_round64(v[i + j] / eff, c);
+      r[j] += d * d;
+    }
+  return ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+}
+
+template <int G>
+__device__ __forceinline__ void load_group(const double* y, int64_t g, double (&v)[G]) {
+  const double2* p = reinterpret_cast<const double2*>(y + g * G);
+#pragma unroll
+  for (int i = 0; i < G / 2; ++i) {
+    const double2 t = p[i];
+    v[2 * i] = t.x;
+    v[2 * i + 1] = t.y;
+  }
+}
+
+// One candidate pass (quantizers.py:288-302) at tensor scale ts = f32(sg * factor).
+template <int G, int FMT>
+__global__ void __launch_bounds__(128) k_mse_pass(const double* __restrict__ y, int64_t ngroups,
+                                                  const double* __restrict__ cand, int ncand,
+                                                  const double* __restrict__ raw0, double sg, double ts,
+                                                  uint8_t* __restrict__ sc, double* __restrict__ dec,
+                                                  double* __restrict__ gerr, uint8_t* __restrict__ codes,
+                                                  uint32_t* status) {
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < ngroups; g += (int64_t)gridDim.x * blockDim.x) {
+    double v[G];
+    load_group<G>(y, g, v);
+    const double r0 = raw0[g];
+    double best = 0.0, bdec = 1.0;
+    uint32_t bcode = 0, bad = 0;
+    for (int c = 0; c < ncand; ++c) {
+      const double enc = (cand[c] * r0) / sg;
+      uint32_t code;
+      double d;
+      if constexpr (FMT == MRFP4_FMT_MXFP4) {
+        const double e = fmin(fmax(rint(log2(enc)), -127.0), 127.0);   // formats.py:225
+        code = (uint32_t)(e + 127.0);
+        d = ldexp(1.0, (int)e);
+      } else {
+        code = e4m3_code64(enc);
+        d = e4m3_value64(code);
+      }
+      const double eff = ts * d;
+      if (!(eff > 0.0)) {   // B / 0: the reference raises DataError (fp4_round_codes, formats.py:101-102)
+        bad |= MRFP4_STATUS_SCALE_UNDERFLOW;
+        continue;
+      }
+      const double err = group_err<G>(v, eff);
+      if (!(err <= 1.79e308)) bad |= MRFP4_STATUS_NONFINITE;
+      if (c == 0 || err < best) {
+        best = err;
+        bcode = code;
+        bdec = d;
+      }
+    }
+    sc[g] = (uint8_t)bcode;
+    dec[g] = bdec;
+    gerr[g] = best;
+    const double eff = ts * bdec;
+#pragma unroll
+    for (int i = 0; i < G; i += 2) {
+      uint32_t c0, c1;
+      fp4_round64(v[i] / eff, c0);
+      fp4_round64(v[i + 1] / eff, c1);
+      codes[g * (G / 2) + i / 2] = (uint8_t)(c0 | (c1 << 4));
+    }
+    if (bad) atomicOr(status, bad);
+  }
+}
+
+// Group errors at a fixed assignment (quantizers.py:304-306, total_err's per-group terms).
+template <int G>
+__global__ void __launch_bounds__(128) k_mse_group_err(const double* __restrict__ y, int64_t ngroups,
+                                                       const double* __restrict__ dec, double ts,
+                                                       double* __restrict__ gerr, uint32_t* status) {
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < ngroups; g += (int64_t)gridDim.x * blockDim.x) {
+    double v[G];
+    load_group<G>(y, g, v);
+    const double eff = ts * dec[g];
+    if (!(eff > 0.0)) {
+      atomicOr(status, MRFP4_STATUS_SCALE_UNDERFLOW);
+      gerr[g] = 0.0;
+      continue;
+    }
+    gerr[g] = group_err<G>(v, eff);
+  }
+}
+
+int grid_for(int64_t n) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 128), (int64_t)sms * 16));
+}
+
+}  // namespace
+
+int launch_mse_pass(const double* y, int64_t ngroups, int fmt, const double* cand, int ncand, const double* raw0,
+                    double sg, double ts, uint8_t* sc, double* dec, double* gerr, uint8_t* codes, uint32_t* status,
+                    cudaStream_t s) {
+  const int grid = grid_for(ngroups);
+  if (fmt == MRFP4_FMT_MXFP4)
+    k_mse_pass<32, MRFP4_FMT_MXFP4><<<grid, 128, 0, s>>>(y, ngroups, cand, ncand, raw0, sg, ts, sc, dec, gerr, codes,
+                                                          status);
+  else
+    k_mse_pass<16, MRFP4_FMT_NVFP4><<<grid, 128, 0, s>>>(y, ngroups, cand, ncand, raw0, sg, ts, sc, dec, gerr, codes,
+                                                          status);
+  return cudaPeekAtLastError() == cudaSuccess ? MRFP4_OK : MRFP4_ECUDA;
+}
+
+int launch_mse_group_err(const double* y, int64_t ngroups, int fmt, const double* dec, double ts, double* gerr,
+                         uint32_t* status, cudaStream_t s) {
+  const int grid = grid_for(ngroups);
+  if (fmt == MRFP4_FMT_MXFP4)
+    k_mse_group_err<32><<<grid, 128, 0, s>>>(y, ngroups, dec, ts, gerr, status);
+  else
+    k_mse_group_err<16><<<grid, 128, 0, s>>>(y, ngroups, dec, ts, gerr, status);
+  return cudaPeekAtLastError() == cudaSuccess ? MRFP4_OK : MRFP4_ECUDA;
+}
+
+}  // namespace mrfp4

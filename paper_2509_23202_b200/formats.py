@@ -186,3 +186,20 @@ def pack_tensor(element_codes, scale_codes, spec: FormatSpec, dims=None, tensor_
 
 def unpack_tensor(t) -> tuple[np.ndarray, np.ndarray]:
     return unpack_codes(t.codes, t.rows * t.cols).reshape(t.rows, t.cols), np.array(t.scale_codes, copy=True)
+
+
+class ScaleMode(enum.Enum):
+    """How group scales are chosen (quantizers.py:42-44)."""
+
+    ABSMAX = "absmax"
+    MSE = "mse"
+
+
+@dataclasses.dataclass(frozen=True)
+class ScalePolicy:
+    """Scale policy with the reference's fields (quantizers.py:47-59).  ``scale_fit`` (fitted
+    E8M0 grid) has no hardware encoding and is rejected by the GPU path."""
+
+    mode: ScaleMode = ScaleMode.ABSMAX
+    e8m0_four_thirds: bool = True
+    scale_fit: tuple | str | None = None

@@ -27,16 +27,18 @@ from .transforms import hadamard_block, transform_for
 _DT = {torch.bfloat16: _lib.DT_BF16, torch.float16: _lib.DT_F16, torch.float32: _lib.DT_F32}
 
 
-def _check_policy(policy, fmt: int) -> None:
+def _is_mse(policy) -> bool:
+    return getattr(getattr(policy, "mode", None), "value", "absmax") == "mse"
+
+
+def _check_policy(policy, fmt: int, mse: bool = False) -> None:
+    """Policies the GPU path encodes; ``policy.mode`` is ignored by quantize_rtn, as in the
+    reference (quantizers.py:247-255), and dispatched by ``quantize`` (:341-347)."""
     if policy is None:
         return
-    mode = getattr(getattr(policy, "mode", None), "value", "absmax")
-    if mode != "absmax":
-        raise DataError("unsupported on GPU path: ScaleMode.MSE (offline weight-only search, "
-                        "quantizers.py:263-327); quantize weights with the reference and use prepare_weight")
     if getattr(policy, "scale_fit", None) is not None:
         raise DataError("unsupported on GPU path: scale_fit (fitted E8M0 grid is not hardware E8M0)")
-    if fmt != FMT_NVFP4 and not getattr(policy, "e8m0_four_thirds", True):
+    if fmt != FMT_NVFP4 and not getattr(policy, "e8m0_four_thirds", True) and not mse:
         raise DataError("unsupported on GPU path: e8m0_four_thirds=False")
 
 
@@ -197,5 +199,124 @@ def quantize_rtn(X, spec, policy=None, transform=None, *, check: bool = True) ->
 
 
 def quantize(X, spec, policy=None, transform=None, *, check: bool = True) -> GpuQuantResult:
-    """``microfp.quantize`` dispatch (quantizers.py:341-347); MSE mode is offline-only."""
+    """``microfp.quantize`` dispatch (quantizers.py:341-347): ScaleMode.MSE runs the MSE scale
+    search (``mse_optimize_scales``) on the GPU, anything else is ``quantize_rtn``."""
+    if _is_mse(policy):
+        return mse_optimize_scales(X, spec, transform=transform, policy=policy)
     return quantize_rtn(X, spec, policy=policy, transform=transform, check=check)
+
+
+MSE_SEARCH_MULTIPLIERS = np.linspace(0.50, 1.20, 128)   # quantizers.py:36-39
+MSE_SEARCH_ROUNDS = 3
+MSE_SEARCH_RTOL = 1e-12
+_CHUNK_GROUPS = 2048
+
+
+def rotate_f64(X: torch.Tensor, had_k: int) -> torch.Tensor:
+    """apply_blockwise (transforms.py:77-91) in float64 on the GPU: the integer Hadamard sums
+    are exact (cuBLAS DGEMM of +-1 against bf16 / fp16 / fp32 inputs), then one rounding by
+    RN64(1 / RN64(sqrt(k))), the same y = RN64(S * c) the K1 kernels decide on."""
+    Xd = X.to(torch.float64)
+    if not had_k:
+        return Xd.contiguous()
+    M, K = Xd.shape
+    idx = torch.arange(had_k, device=X.device)
+    par = torch.zeros((had_k, had_k), dtype=torch.int64, device=X.device)
+    a = idx[:, None] & idx[None, :]
+    while bool(a.any()):
+        par ^= a & 1
+        a = a >> 1
+    H = (1 - 2 * par).to(torch.float64)
+    return torch.matmul(Xd.view(M, K // had_k, had_k), H).mul_(1.0 / float(np.sqrt(had_k))).view(M, K)
+
+
+def mse_optimize_scales(X, spec, transform=None, policy=None) -> GpuQuantResult:
+    """``quantize_rtn`` with MSE-optimised scales on the GPU (quantizers.py:330-337,
+    ``optimize_group_scales`` :263-327).
+
+    Same alternating search as the reference: a pass picks, per group, the best of the
+    absmax scale and 128 multipliers in [0.5, 1.2] (each rounded through the scale codec;
+    ties keep the earliest); for NVFP4 the tensor scale is then scanned over the same 128
+    multipliers; at most 3 rounds, stopping at a relative improvement < 1e-12.  Group scores
+    are computed by ``mrfp4_mse_pass`` / ``mrfp4_mse_group_err`` in float64 with numpy's
+    summation order, and their totals are summed with numpy, so the decisions are the
+    reference's.  Raises ``DataError`` where the reference does (non-finite input; a candidate
+    scale that decodes to 0)."""
+    fmt = format_code(spec)
+    _check_policy(policy, fmt, mse=True)
+    had_k = hadamard_block(transform)
+    X = as_device_matrix(X)
+    M, K = X.shape
+    G = GROUP[fmt]
+    if K % G:
+        raise DataError(f"columns ({K}) not divisible by group size ({G})")
+    if had_k and K % had_k:
+        raise DataError(f"columns ({K}) not divisible by transform block ({had_k})")
+    if not bool(torch.isfinite(X).all()):                                  # quantizers.py:99-100
+        raise DataError("non-finite element")
+    dev = X.device
+    L = _lib.lib()
+    stream = _lib.stream_ptr(torch, dev)
+    Y = rotate_f64(X, had_k)
+    ng = M * K // G
+    B = Y.view(ng, G)
+    absmax = B.abs().amax(dim=1)
+    raw0 = torch.where(absmax == 0, torch.ones_like(absmax), absmax / 6.0).contiguous()
+    is_global = fmt == FMT_NVFP4
+    s_global, factor = 1.0, 1.0
+    if is_global:                                                         # quantizers.py:195-200
+        top = float(absmax.max()) / 6.0
+        s_global = float(np.float32(top / 448.0)) if top > 0 else 1.0
+    elif getattr(policy, "e8m0_four_thirds", True) if policy is not None else True:
+        factor = 4.0 / 3.0
+    cand_np = np.concatenate([[1.0], MSE_SEARCH_MULTIPLIERS])
+    cand = torch.from_numpy(cand_np).to(dev)
+    sc = torch.empty(ng, dtype=torch.uint8, device=dev)
+    dec = torch.empty(ng, dtype=torch.float64, device=dev)
+    gerr = torch.empty(ng, dtype=torch.float64, device=dev)
+    gerr2 = torch.empty(ng, dtype=torch.float64, device=dev)
+    codes = torch.empty((M, K // 2), dtype=torch.uint8, device=dev)
+    scratch = torch.zeros(12, dtype=torch.int32, device=dev)
+    status = _lib.ptr(scratch)
+
+    def pass_groups(sg: float) -> float:
+        ts = float(np.float32(sg * factor))
+        _lib.check(L.mrfp4_mse_pass(_lib.ptr(Y), ng, fmt, _lib.ptr(cand), len(cand_np), _lib.ptr(raw0), sg, ts,
+                                    _lib.ptr(sc), _lib.ptr(dec), _lib.ptr(gerr), _lib.ptr(codes), status, stream))
+        errs = gerr.cpu().numpy()
+        total = 0.0
+        for lo in range(0, ng, _CHUNK_GROUPS):
+            total += float(errs[lo:lo + _CHUNK_GROUPS].sum())
+        return total
+
+    def total_err(sg: float) -> float:
+        ts = float(np.float32(sg * factor))
+        _lib.check(L.mrfp4_mse_group_err(_lib.ptr(Y), ng, fmt, _lib.ptr(dec), ts, _lib.ptr(gerr2), status, stream))
+        return float(gerr2.cpu().numpy().sum())
+
+    best_total = pass_groups(s_global)
+    for _ in range(MSE_SEARCH_ROUNDS):
+        if is_global:
+            anchor, improved_to = s_global, best_total
+            for m in cand_np[1:]:
+                sg_c = float(np.float32(m * anchor))
+                if sg_c > 0:
+                    e = total_err(sg_c)
+                    if e < improved_to:
+                        improved_to, s_global = e, sg_c
+        improved_to = pass_groups(s_global)
+        if best_total - improved_to < MSE_SEARCH_RTOL * max(best_total, 1e-300):
+            best_total = improved_to
+            break
+        best_total = improved_to
+    st = int(scratch[0].item())
+    if st & _lib.STATUS_SCALE_UNDERFLOW:
+        raise DataError("non-finite element (a candidate group scale underflows the scale format)")
+    if st & _lib.STATUS_NONFINITE:
+        raise DataError("non-finite element")
+    res = alloc_result(M, K, fmt, had_k, dev)
+    res.codes.copy_(codes)
+    _lib.check(L.mrfp4_sf_swizzle(_lib.ptr(sc), _lib.ptr(res.sf), M, K // G, stream))
+    res.tensor_scale_dev.fill_(float(np.float32(s_global * factor)))
+    res.source = X
+    return res

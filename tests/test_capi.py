@@ -86,3 +86,13 @@ def test_no_cuda_path_is_loud():
     import paper_2509_23202_b200 as P
     with pytest.raises(RuntimeError, match="CUDA"):
         P.quantize_rtn(np.zeros((2, 32)), P.FormatSpec.mxfp4())
+
+
+def test_mse_entry_points_reject_bad_arguments():
+    L = _lib.lib()
+    nul = None
+    assert L.mrfp4_mse_pass(nul, 10, 9, nul, 129, nul, 1.0, 1.0, nul, nul, nul, nul, nul, nul) == _lib.EUNSUPPORTED
+    assert L.mrfp4_mse_pass(nul, 0, 1, nul, 129, nul, 1.0, 1.0, nul, nul, nul, nul, nul, nul) == _lib.EINVAL
+    assert L.mrfp4_mse_pass(nul, 10, 1, nul, 129, nul, 0.0, 1.0, nul, nul, nul, nul, nul, nul) == _lib.EINVAL
+    assert L.mrfp4_mse_pass(nul, 10, 1, nul, 129, nul, 1.0, 1.0, nul, nul, nul, nul, nul, nul) == _lib.EINVAL
+    assert L.mrfp4_mse_group_err(nul, 10, 0, nul, -1.0, nul, nul, nul) == _lib.EINVAL
