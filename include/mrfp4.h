@@ -133,6 +133,20 @@ int mrfp4_dequantize(const uint8_t* codes, const uint8_t* sf, const float* tenso
                      int64_t rows, int64_t cols, int fmt, float* out, void* stream);
 
 /*
+ * K2 with the NEXT layer's act-quant fused into its epilogue: computes
+ * Y = bf16(a . b^T) as mrfp4_gemm does and, from those bf16 values, the MXFP4 quantization
+ * quantize_rtn(Y, FormatSpec.mxfp4(), transform=hadamard(next_had_k)) (quantizers.py:247-255)
+ * -- E2M1 codes [M, N/2], swizzled E8M0 scales [M, N/32] (padding rows zeroed) and the tensor
+ * scale f32(4/3) -- bit-identical to mrfp4_act_quant on Y.  y_bf16 may be NULL (Y not stored).
+ * Requires M > 128, K % 256 == 0, N % 128 == 0, next_had_k in {0, 16, 32}; status: bit 1 =
+ * non-finite Y.  MXFP4 only: NVFP4's tensor scale needs the whole Y before any group is encoded.
+ */
+int mrfp4_gemm_quant_next(const uint8_t* a, const uint8_t* a_sf, const float* a_ts, const uint8_t* b,
+                          const uint8_t* b_sf, const float* b_ts, void* y_bf16, int64_t ldy, int64_t M, int64_t N,
+                          int64_t K, int fmt, int next_had_k, uint8_t* next_codes, uint8_t* next_sf,
+                          float* next_tensor_scale, uint32_t* status, void* stream);
+
+/*
  * Offline MSE scale search (replaces the numpy loops of
  * optimize_group_scales, quantizers.py:263-327).  y: the rotated matrix in float64, viewed as
  * ngroups contiguous groups of 32 (MXFP4) / 16 (NVFP4) values, 16-byte aligned.

@@ -23,6 +23,10 @@ int launch_sf_swizzle(const uint8_t* src, uint8_t* dst, int64_t rows, int64_t co
 int launch_sf_unswizzle(const uint8_t* src, uint8_t* dst, int64_t rows, int64_t cols, cudaStream_t s);
 int launch_dequantize(const uint8_t* codes, const uint8_t* sf, const float* ts, int64_t rows, int64_t cols, int fmt,
                       float* out, cudaStream_t s);
+int launch_gemm_quant_next(const uint8_t* a, const uint8_t* a_sf, const float* a_ts, const uint8_t* b,
+                           const uint8_t* b_sf, const float* b_ts, void* y, int64_t ldy, int64_t M, int64_t N,
+                           int64_t K, int fmt, int next_hk, uint8_t* q_codes, uint8_t* q_sf, float* q_ts,
+                           uint32_t* q_status, cudaStream_t s);
 int launch_mse_pass(const double* y, int64_t ngroups, int fmt, const double* cand, int ncand, const double* raw0,
                     double sg, double ts, uint8_t* sc, double* dec, double* gerr, uint8_t* codes, uint32_t* status,
                     cudaStream_t s);
@@ -199,4 +203,25 @@ int mrfp4_mse_group_err(const double* y, int64_t ngroups, int fmt, const double*
   return cuda_status(mrfp4::launch_mse_group_err(y, ngroups, fmt, decoded, ts, group_err, status,
                                                  static_cast<cudaStream_t>(stream)),
                      "mrfp4_mse_group_err");
+}
+
+int mrfp4_gemm_quant_next(const uint8_t* a, const uint8_t* a_sf, const float* a_ts, const uint8_t* b,
+                          const uint8_t* b_sf, const float* b_ts, void* y_bf16, int64_t ldy, int64_t M, int64_t N,
+                          int64_t K, int fmt, int next_had_k, uint8_t* next_codes, uint8_t* next_sf,
+                          float* next_tensor_scale, uint32_t* status, void* stream) {
+  if (mrfp4_group_size(fmt) == 0) return fail(MRFP4_EUNSUPPORTED, "unknown format %d", fmt);
+  if (M < 1 || N < 1 || K < 1) return fail(MRFP4_EINVAL, "empty GEMM");
+  if (M <= 128 || K % 256)
+    return fail(MRFP4_EUNSUPPORTED, "fused next-layer quantization needs M > 128 and K %% 256 == 0 (2-CTA GEMM)");
+  if (N % 128) return fail(MRFP4_EUNSUPPORTED, "fused next-layer quantization needs N %% 128 == 0");
+  if (next_had_k != 0 && next_had_k != 16 && next_had_k != 32)
+    return fail(MRFP4_EUNSUPPORTED, "fused next-layer quantization: Hadamard block must be 0, 16 or 32");
+  if (y_bf16 && (ldy < N || ldy % 16)) return fail(MRFP4_EINVAL, "bad output row stride");
+  if (!a || !a_sf || !a_ts || !b || !b_sf || !b_ts || !next_codes || !next_sf || !next_tensor_scale || !status)
+    return fail(MRFP4_EINVAL, "null buffer");
+  if (!aligned(next_codes, 16)) return fail(MRFP4_EUNSUPPORTED, "codes must be 16-byte aligned");
+  return cuda_status(mrfp4::launch_gemm_quant_next(a, a_sf, a_ts, b, b_sf, b_ts, y_bf16, ldy, M, N, K, fmt,
+                                                   next_had_k, next_codes, next_sf, next_tensor_scale, status,
+                                                   static_cast<cudaStream_t>(stream)),
+                     "mrfp4_gemm_quant_next");
 }

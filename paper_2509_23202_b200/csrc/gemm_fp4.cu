@@ -20,10 +20,13 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cmath>
+#include <type_traits>
 #include <cstring>
 #include <mutex>
 
 #include "common.cuh"
+#include "quant_core.cuh"
 #include "sm100.cuh"
 
 namespace mrfp4 {
@@ -78,7 +81,24 @@ struct GemmArgs {
   size_t ws_bytes;
   unsigned long long* dbg;  // perf experiments: per-k-block MMA-thread timestamps of CTA 0
   int debug;  // perf experiments: 1 = no operand loads, 2 = no MMAs (0 in production)
+  // Fused next-layer MXFP4 quantization of the bf16 output (OUT == kOutMxq, 2-CTA kernel):
+  // the epilogue rounds each output row to bf16, rotates it by H_k (k = q_hk in {0, 16, 32})
+  // and writes the next layer's E2M1 codes [M, N/2] + swizzled E8M0 scales, exactly what K1
+  // would produce from the bf16 output (quantizers.py:247-255).  d (bf16 Y) may be null.
+  uint8_t* q_codes;
+  uint8_t* q_sf;
+  float* q_ts;        // the next layer's tensor scale: f32(4/3) (quantizers.py:191, :206-207)
+  uint32_t* q_status;
+  uint32_t q_cb;      // scale column blocks of the next layer: N / 32 / 4
+  int64_t q_rows_pad; // ceil(M / 128) * 128
+  qc::AQParams qp;    // c64 / kraw / kmx / pm of the next layer's rotation
 };
+constexpr int kOutMxq = 100;  // internal OUT tag (not an ABI dtype)
+
+// Swizzled scale-factor offset (128 x 4 atoms), 32-bit.
+__device__ __forceinline__ uint32_t sf_off32q(uint32_t r, uint32_t c, uint32_t cb) {
+  return ((r >> 7) * cb + (c >> 2)) * 512u + (r & 31u) * 16u + ((r >> 5) & 3u) * 4u + (c & 3u);
+}
 
 
 
@@ -476,6 +496,42 @@ __device__ __forceinline__ void issue_stage_tail(int nk, uint32_t el, uint32_t d
   }
 }
 
+// Next-layer MXFP4 quantization of one output row's 128 bf16 columns (4 groups of 32) --
+// the K1 arithmetic (quant_core.cuh) on the values K1 would read back from Y.  Padding rows
+// [M, rows_pad) get zero scale bytes, as K1 writes them.
+template <int HKQ>
+__device__ __forceinline__ void quant_next_row(const GemmArgs& g, int64_t row, int64_t col0, const uint32_t (&pkd)[64]) {
+  using namespace qc;
+  if (row >= g.M) {
+    if (row < g.q_rows_pad)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) g.q_sf[sf_off32q((uint32_t)row, (uint32_t)((col0 >> 5) + c), g.q_cb)] = 0;
+    return;
+  }
+  uint32_t bad = 0;
+#pragma unroll 1
+  for (int c = 0; c < 4; ++c) {
+    u64 P[kPairs];
+#pragma unroll
+    for (int j = 0; j < kPairs; ++j) {
+      const uint32_t w = pkd[16 * c + j];
+      P[j] = pk(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
+    }
+    if constexpr (HKQ > 0) fwht<HKQ>(P, 0, g.qp.pm);
+    float a0, a1;
+    half_amax(P, a0, a1);
+    const float a = max3n(a0, a1, 0.f);
+    if (__float_as_uint(a) >= 0x7f800000u) bad |= MRFP4_STATUS_NONFINITE;
+    const GroupScale s0 = mx_group_scale(a, g.qp);
+    uint32_t w4[4];
+    quantize_seg(P, s0, s0, 1.33333337306976318359375f, g.qp, w4);
+    *reinterpret_cast<uint4*>(g.q_codes + row * (g.N >> 1) + ((col0 + 32 * c) >> 1)) =
+        make_uint4(w4[0], w4[1], w4[2], w4[3]);
+    g.q_sf[sf_off32q((uint32_t)row, (uint32_t)((col0 >> 5) + c), g.q_cb)] = (uint8_t)s0.code;
+  }
+  if (bad) atomic_or_status(g.q_status, bad);
+}
+
 // Work of one cluster, identical for all roles of both CTAs: whole 256 x 256 tiles,
 // tile = cluster + i * clusters (m-block fastest, so concurrent pairs share weight panels in L2).
 // (A stream-K tail -- splitting a sparse last wave's k-stages across pairs with fp32
@@ -507,7 +563,7 @@ struct Ring {
   }
 };
 
-template <int VEC, int OUT>
+template <int VEC, int OUT, int HKQ = 0>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(448, 1)
     k_gemm_fp4_2sm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs g) {
   using C = Cfg2<VEC>;
@@ -728,6 +784,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(448, 1)
     const int q = warp & 3, h = (warp - 6) >> 2;
     pdl_wait();
     const float alpha = __ldg(g.a_ts) * __ldg(g.b_ts);
+    if constexpr (OUT == kOutMxq)
+      if (blockIdx.x == 0 && warp == 6 && lane == 0) *g.q_ts = 1.33333337306976318359375f;
     uint32_t acc_phase = 0;
     auto release_acc = [&] {
       sm100::tc_fence_before();
@@ -747,7 +805,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(448, 1)
       const int64_t row = (int64_t)m_blk * 256 + rank * 128 + q * 32 + lane;
       const int64_t col0 = (int64_t)n_blk * 256 + h * 128;
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + h * 128;
-      if constexpr (OUT == MRFP4_DT_BF16) {
+      if constexpr (OUT == MRFP4_DT_BF16 || OUT == kOutMxq) {
         uint32_t pkd[64];
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
@@ -761,6 +819,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(448, 1)
           }
         }
         release_acc();
+        if constexpr (OUT == kOutMxq) {
+          if (col0 < g.N) quant_next_row<HKQ>(g, row, col0, pkd);
+          if (!g.d) continue;
+        }
         if (row < g.M) {
           __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(g.d) + row * g.ldd + col0;
           // 32-B stores: whole L2 sectors per lane (16-B stores from 32 rows at once were
@@ -907,12 +969,12 @@ int launch(const uint8_t* a, const uint8_t* b, const GemmArgs& args0, cudaStream
   return MRFP4_OK;
 }
 
-template <int VEC, int OUT>
+template <int VEC, int OUT, int HKQ = 0>
 int launch2(const uint8_t* a, const uint8_t* b, const GemmArgs& args0, cudaStream_t s) {
   using C = Cfg2<VEC>;
   static bool attr_set = false;
   if (!attr_set) {
-    if (cudaFuncSetAttribute(k_gemm_fp4_2sm<VEC, OUT>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem) !=
+    if (cudaFuncSetAttribute(k_gemm_fp4_2sm<VEC, OUT, HKQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem) !=
         cudaSuccess)
       return MRFP4_ECUDA;
     attr_set = true;
@@ -931,7 +993,7 @@ int launch2(const uint8_t* a, const uint8_t* b, const GemmArgs& args0, cudaStrea
   const int tiles = g.num_m_blk * g.num_n_blk;
   int nclu = std::min(tiles, num_sms() / 2);
   if (g_force_grid > 0) nclu = std::min(nclu, std::max(1, g_force_grid / 2));
-  return launch_pdl(k_gemm_fp4_2sm<VEC, OUT>, dim3(2 * nclu), dim3(C::kThreads2), C::kSmem, s, tmA, tmB, g) ==
+  return launch_pdl(k_gemm_fp4_2sm<VEC, OUT, HKQ>, dim3(2 * nclu), dim3(C::kThreads2), C::kSmem, s, tmA, tmB, g) ==
                  cudaSuccess
              ? MRFP4_OK
              : MRFP4_ECUDA;
@@ -997,6 +1059,46 @@ int launch_gemm_fp4(const uint8_t* a, const uint8_t* a_sf, const float* a_ts, co
   }
   return d_dtype == MRFP4_DT_BF16 ? launch<32, 256, MRFP4_DT_BF16>(a, b, g, s)
                                   : launch<32, 256, MRFP4_DT_F32>(a, b, g, s);
+}
+
+// K2 with the next layer's MXFP4 act-quant fused into the epilogue (2-CTA kernel only).
+int launch_gemm_quant_next(const uint8_t* a, const uint8_t* a_sf, const float* a_ts, const uint8_t* b,
+                           const uint8_t* b_sf, const float* b_ts, void* y, int64_t ldy, int64_t M, int64_t N,
+                           int64_t K, int fmt, int next_hk, uint8_t* q_codes, uint8_t* q_sf, float* q_ts,
+                           uint32_t* q_status, cudaStream_t s) {
+  GemmArgs g{};
+  g.b = b;
+  g.preissue = g_preissue;
+  g.a_sf = a_sf;
+  g.b_sf = b_sf;
+  g.a_ts = a_ts;
+  g.b_ts = b_ts;
+  g.d = y;
+  g.M = M;
+  g.N = N;
+  g.K = K;
+  g.ldd = y ? ldy : N;
+  g.q_codes = q_codes;
+  g.q_sf = q_sf;
+  g.q_ts = q_ts;
+  g.q_status = q_status;
+  g.q_cb = (uint32_t)(N / 128);
+  g.q_rows_pad = ceil_div(M, 128) * 128;
+  const double c64 = next_hk ? 1.0 / std::sqrt((double)next_hk) : 1.0;
+  g.qp.c64 = c64;
+  g.qp.kraw = (float)(c64 / 6.0);
+  g.qp.kmx = (float)(c64 / (double)1.33333337306976318359375f);
+  const float pm[2] = {1.f, -1.f};
+  memcpy(&g.qp.pm, pm, sizeof(pm));
+  auto go = [&](auto vec_tag) {
+    constexpr int V = decltype(vec_tag)::value;
+    switch (next_hk) {
+      case 16: return launch2<V, kOutMxq, 16>(a, b, g, s);
+      case 32: return launch2<V, kOutMxq, 32>(a, b, g, s);
+      default: return launch2<V, kOutMxq, 0>(a, b, g, s);
+    }
+  };
+  return fmt == MRFP4_FMT_NVFP4 ? go(std::integral_constant<int, 16>{}) : go(std::integral_constant<int, 32>{});
 }
 
 }  // namespace mrfp4

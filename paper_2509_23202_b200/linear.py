@@ -27,7 +27,7 @@ import torch
 
 from . import _lib
 from .errors import DataError
-from .formats import FMT_NVFP4 as FMT_NVFP4_CODE, GROUP, format_code, spec_for
+from .formats import FMT_MXFP4 as FMT_MXFP4_CODE, FMT_NVFP4 as FMT_NVFP4_CODE, GROUP, format_code, spec_for
 from .quantize import GpuQuantResult, act_quant_into, alloc_result, as_device_matrix, quantize_rtn
 from .transforms import hadamard_block, transform_for
 
@@ -274,3 +274,34 @@ def quantized_linear_host(x: torch.Tensor, w: PackedWeight, *, out: torch.Tensor
     cur.wait_event(ev_out[max(ev_out)])
     cur.wait_event(ev_comp[max(ev_comp)])
     return out
+
+
+def quantized_linear_requant(x, w: PackedWeight, next_transform=None, *, keep_output: bool = False,
+                             check: bool = False):
+    """``quantized_linear`` whose bf16 output is quantized for the NEXT layer in K2's epilogue
+    (SURVEY.md 8(f) row f4): returns the GpuQuantResult that
+    ``quantize_rtn(y, FormatSpec.mxfp4(), transform=next_transform)`` would return for
+    y = quantized_linear(x, w) -- bit-identical -- without writing y to HBM and reading it back
+    (``keep_output=True`` also returns y).  MXFP4 only (NVFP4's tensor scale is a max over all
+    of y); next_transform: None or a Hadamard block of 16 / 32."""
+    if not isinstance(w, PackedWeight):
+        w = prepare_weight(w)
+    x2 = as_device_matrix(x, w.device)
+    M, K = x2.shape
+    if K != w.K:
+        raise DataError(f"activation K={K} does not match weight K={w.K}")
+    hk = hadamard_block(next_transform)
+    a = alloc_result(M, K, w.fmt, w.had_k, x2.device)
+    act_quant_into(x2, w.fmt, w.had_k, a.codes, a.sf, a.tensor_scale_dev, a.scratch)
+    res = alloc_result(M, w.N, FMT_MXFP4_CODE, hk, x2.device)
+    y = torch.empty((M, w.N), dtype=torch.bfloat16, device=x2.device) if keep_output else None
+    L = _lib.lib()
+    _lib.check(L.mrfp4_gemm_quant_next(
+        _lib.ptr(a.codes), _lib.ptr(a.sf), _lib.ptr(a.tensor_scale_dev),
+        _lib.ptr(w.codes), _lib.ptr(w.sf), _lib.ptr(w.tensor_scale_dev),
+        _lib.ptr(y) if y is not None else None, w.N, M, w.N, K, w.fmt, hk,
+        _lib.ptr(res.codes), _lib.ptr(res.sf), _lib.ptr(res.tensor_scale_dev), _lib.ptr(res.scratch),
+        _lib.stream_ptr(torch, x2.device)))
+    if check:
+        res.check()
+    return (res, y) if keep_output else res

@@ -195,3 +195,36 @@ def test_host_pipeline_matches_device_call(fmt, k, M):
     P.quantized_linear_host(X, w, out=out)
     torch.cuda.synchronize()
     assert torch.equal(out, P.quantized_linear(X.cuda(), w, out_dtype=torch.float32).cpu())
+
+
+@pytest.mark.parametrize("fmt", ["mxfp4", "nvfp4"])
+@pytest.mark.parametrize("M,N,K", [(2048, 4096, 2048), (300, 640, 1024), (129, 1152, 512)])
+@pytest.mark.parametrize("next_k", [0, 16, 32])
+def test_requant_epilogue_matches_act_quant(fmt, M, N, K, next_k):
+    """K2 with the next layer's MXFP4 act-quant in its epilogue == quantize_rtn of the bf16
+    output, byte for byte (codes, swizzled scales incl. zero padding rows, tensor scale)."""
+    rng = np.random.default_rng(M + N + next_k)
+    X = torch.from_numpy(O.bf16_round(rng.standard_normal((M, K)))).cuda().bfloat16()
+    W = torch.from_numpy(O.bf16_round(rng.standard_normal((N, K)) / np.sqrt(K))).cuda().bfloat16()
+    w = P.quantize_weight(W, SPEC[fmt], P.TransformSpec.hadamard(16))
+    tr = P.TransformSpec.hadamard(next_k) if next_k else None
+    q, y = P.quantized_linear_requant(X, w, tr, keep_output=True, check=True)
+    y_ref = P.quantized_linear(X, w)
+    assert torch.equal(y, y_ref)
+    ref = P.quantize_rtn(y_ref, SPEC["mxfp4"], transform=tr)
+    assert torch.equal(q.codes, ref.codes) and torch.equal(q.sf, ref.sf)
+    assert q.tensor_scale == ref.tensor_scale
+    q2 = P.quantized_linear_requant(X, w, tr)          # without storing y
+    assert torch.equal(q2.codes, ref.codes) and torch.equal(q2.sf, ref.sf)
+
+
+def test_requant_rejects_unsupported():
+    rng = np.random.default_rng(1)
+    X = torch.from_numpy(O.bf16_round(rng.standard_normal((64, 512)))).cuda().bfloat16()   # M <= 128
+    W = torch.from_numpy(O.bf16_round(rng.standard_normal((256, 512)) / 23)).cuda().bfloat16()
+    w = P.quantize_weight(W, SPEC["mxfp4"], P.TransformSpec.hadamard(32))
+    with pytest.raises(P.DataError):
+        P.quantized_linear_requant(X, w)
+    X2 = torch.from_numpy(O.bf16_round(rng.standard_normal((256, 512)))).cuda().bfloat16()
+    with pytest.raises(P.DataError):
+        P.quantized_linear_requant(X2, w, P.TransformSpec.hadamard(128))
