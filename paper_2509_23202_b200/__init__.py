@@ -11,6 +11,7 @@ for everything on the path ``Q(X H_k) Q(W H_k)^T``:
     quantized_linear                 K1 + K2 (tcgen05 block-scaled FP4 GEMM)
     quantized_linear_host            the same on host buffers, H2D / compute / D2H pipelined
     quantized_linear_requant         K2 + the next layer's MXFP4 act-quant fused in its epilogue
+    GraphedLinear                    a fixed-shape quantized_linear captured into a CUDA graph
     quantized_linear_sharded         N-sharded linear + NCCL all-gather
 
 All compute runs in libmrfp4.so (sm_100a); there is no CPU fallback.
@@ -20,7 +21,7 @@ from .errors import DataError, NumericalError
 from .fileio import parse_quant, quant_bytes, read_quant, write_quant
 from .formats import (FMT_MXFP4, FMT_NVFP4, FormatSpec, MfpTensor, ScaleFormat, ScaleKind, ScaleMode, ScalePolicy,
                       pack_tensor, unpack_tensor)
-from .linear import (PackedWeight, gemm, prepare_weight, quantize_weight, quantized_linear, quantized_linear_host,
+from .linear import (GraphedLinear, PackedWeight, gemm, prepare_weight, quantize_weight, quantized_linear, quantized_linear_host,
                      quantized_linear_requant)
 from .quantize import GpuQuantResult, mse_optimize_scales, quantize, quantize_rtn
 from .transforms import TransformKind, TransformSpec
@@ -31,7 +32,7 @@ __all__ = [
     "DataError", "NumericalError", "FormatSpec", "ScaleFormat", "ScaleKind", "ScaleMode", "ScalePolicy", "MfpTensor",
     "mse_optimize_scales",
     "TransformKind", "TransformSpec", "pack_tensor", "unpack_tensor", "quantize_rtn", "quantize",
-    "GpuQuantResult", "PackedWeight", "prepare_weight", "quantize_weight", "quantized_linear", "quantized_linear_host", "quantized_linear_requant", "gemm",
+    "GpuQuantResult", "PackedWeight", "prepare_weight", "quantize_weight", "quantized_linear", "quantized_linear_host", "quantized_linear_requant", "GraphedLinear", "gemm",
     "quantized_linear_sharded", "read_quant", "write_quant", "parse_quant", "quant_bytes",
     "FMT_MXFP4", "FMT_NVFP4",
 ]

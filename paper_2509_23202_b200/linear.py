@@ -305,3 +305,46 @@ def quantized_linear_requant(x, w: PackedWeight, next_transform=None, *, keep_ou
     if check:
         res.check()
     return (res, y) if keep_output else res
+
+
+class GraphedLinear:
+    """``quantized_linear`` for one fixed batch size, captured once into a CUDA graph.
+
+    Decode-sized layers are launch-bound: K1, K2 (and the split-K reduce) cost a few
+    microseconds of GPU time each but tens of microseconds of host work per call through
+    Python.  ``GraphedLinear(w, M)`` records the whole layer (static input / output buffers,
+    PDL edges kept) and ``__call__`` replays it: one graph launch per layer call.
+    """
+
+    def __init__(self, w: PackedWeight, M: int, *, x_dtype=torch.bfloat16, out_dtype=torch.bfloat16):
+        if out_dtype not in _OUT:
+            raise DataError("out_dtype must be torch.bfloat16 or torch.float32")
+        self.w = w
+        dev = w.device
+        self.x = torch.zeros((M, w.K), dtype=x_dtype, device=dev)
+        self.y = torch.empty((M, w.N), dtype=out_dtype, device=dev)
+        self.a = alloc_result(M, w.K, w.fmt, w.had_k, dev)
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):
+            for _ in range(2):   # warm-up: kernel attributes, tensor maps, GEMM workspace
+                self._run()
+        torch.cuda.current_stream(dev).wait_stream(side)
+        torch.cuda.synchronize(dev)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, stream=side):
+            self._run()
+        torch.cuda.synchronize(dev)
+
+    def _run(self):
+        act_quant_into(self.x, self.w.fmt, self.w.had_k, self.a.codes, self.a.sf, self.a.tensor_scale_dev,
+                       self.a.scratch)
+        gemm(self.a, self.w, self.y)
+
+    def __call__(self, x: torch.Tensor | None = None) -> torch.Tensor:
+        """Replay on the current stream; ``x`` (same shape) is copied into the static input first.
+        Returns the static output buffer (overwritten by the next call)."""
+        if x is not None:
+            self.x.copy_(x, non_blocking=True)
+        self.graph.replay()
+        return self.y

@@ -228,3 +228,18 @@ def test_requant_rejects_unsupported():
     X2 = torch.from_numpy(O.bf16_round(rng.standard_normal((256, 512)))).cuda().bfloat16()
     with pytest.raises(P.DataError):
         P.quantized_linear_requant(X2, w, P.TransformSpec.hadamard(128))
+
+
+@pytest.mark.parametrize("fmt,k,M", [("nvfp4", 16, 16), ("mxfp4", 32, 16), ("nvfp4", 128, 256), ("mxfp4", 32, 512)])
+def test_graphed_linear_matches_eager(fmt, k, M):
+    """The CUDA-graph replay of K1 + K2 (+ split-K reduce) equals the eager call, call after call."""
+    rng = np.random.default_rng(M + k)
+    K, N = 4096, 1024
+    W = torch.from_numpy(O.bf16_round(rng.standard_normal((N, K)) / 64)).cuda().bfloat16()
+    w = P.quantize_weight(W, SPEC[fmt], P.TransformSpec.hadamard(k))
+    g = P.GraphedLinear(w, M)
+    for seed in range(3):
+        X = torch.from_numpy(O.bf16_round(np.random.default_rng(seed).standard_normal((M, K)))).cuda().bfloat16()
+        y = g(X).clone()
+        torch.cuda.synchronize()
+        assert torch.equal(y, P.quantized_linear(X, w))
