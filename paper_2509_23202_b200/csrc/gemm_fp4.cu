@@ -576,7 +576,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(448, 1)
   uint64_t* tsf_empty = sf_empty + C::kSfSlots;                      // TMEM SF slot free (MMAs committed)
   uint64_t* tfull = tsf_empty + C::kSfSlots;
   uint64_t* tempty = tfull + 1;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 1);
+  uint64_t* staged = tempty + 1;                                     // non-leader: its 4 stagers done
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(staged + C::kStages);
 
   const uint32_t rank = sm100::cluster_ctarank();
   const bool leader = rank == 0;
@@ -590,7 +591,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(448, 1)
     sm100::tma_prefetch_desc(&tmA);
     sm100::tma_prefetch_desc(&tmB);
     for (int s = 0; s < C::kStages; ++s) {
-      sm100::mbar_init(&full[s], 9);      // leader producer (A/B bytes) + 4 stager warps x 2 CTAs
+      // leader producer (A/B bytes) + the leader's 4 stager warps + the peer's forwarder
+      sm100::mbar_init(&full[s], 6);
+      sm100::mbar_init(&staged[s], 4);
       sm100::mbar_init(&empty[s], 1);
     }
     for (int s = 0; s < C::kSfSlots; ++s) {
@@ -688,6 +691,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(448, 1)
         pdl_wait();
       }
     }
+  } else if (warp == 1 && !leader) {
+    // ------------------------------------------------- peer SF forwarder (non-leader)
+    // The leader's MMAs read this CTA's scale factors from this CTA's TMEM.  Ordering those
+    // tcgen05.st before the MMAs needs a CLUSTER-scope release: with a cta-scope one the MMAs
+    // measurably read stale scale factors (whole 32-row quadrants of the peer's rows wrong,
+    // 8192 x 16384 -> 53248, tests/test_gpu_fullsize.py).  A cluster-scope release is a
+    // MEMBAR.ALL.GPU, so one thread pays it per stage here, off the stager warps' path: it
+    // collects the 4 local stager arrivals and forwards one arrival to the leader's `full`.
+    if (lane == 0) {
+      Ring ab;
+      WorkIter it(g, cluster, nclusters);
+      Work w;
+      while (it.next(g, w)) {
+        for (int kb = w.kb0; kb < w.kb1; ++kb) {
+          sm100::mbar_wait(&staged[ab.idx], ab.ph);
+          sm100::mbar_arrive_remote(&full[ab.idx], 0);
+          ab.next<C::kStages>();
+        }
+      }
+    }
   } else if (warp == 1) {
     if (leader) {
       // ---------------------------------------------------------- MMA issuer
@@ -706,7 +729,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(448, 1)
       Work w;
       for (; it.next(g, w); ++ntl) {
         if (dbg && ntl < 4) dbg[ntl * 260] = clock64();
-        sm100::mbar_wait(tempty, acc_phase ^ 1);
+        sm100::mbar_wait_cluster(tempty, acc_phase ^ 1);   // both CTAs' epilogues (remote arrivals)
         if (dbg && ntl < 4) dbg[ntl * 260 + 1] = clock64();
         for (int kb = w.kb0; kb < w.kb1; ++kb) {
           sm100::mbar_wait(&full[ab.idx], ab.ph);
@@ -767,10 +790,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(448, 1)
         sm100::tmem_st_wait();
         sm100::tc_fence_before();
         __syncwarp();
-        if (lane == 0) {
-          if (leader) sm100::mbar_arrive(&full[ab.idx]);
-          else sm100::mbar_arrive_remote(&full[ab.idx], 0);
-        }
+        if (lane == 0) sm100::mbar_arrive(leader ? &full[ab.idx] : &staged[ab.idx]);
         ab.next<C::kStages>();
         sf.next<C::kSfSlots>();
       }
@@ -792,7 +812,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(448, 1)
       __syncwarp();
       if (lane == 0) {
         if (leader) sm100::mbar_arrive(tempty);
-        else sm100::mbar_arrive_remote(tempty, 0);
+        else sm100::mbar_arrive_remote_relaxed(tempty, 0);
       }
     };
     WorkIter it(g, cluster, nclusters);
