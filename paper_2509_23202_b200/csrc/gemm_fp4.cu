@@ -553,6 +553,28 @@ struct WorkIter {
   }
 };
 
+// Flattened (tile, k-stage) sequence of one cluster's work.
+struct StageIter {
+  WorkIter it;
+  Work w;
+  int kb, nm;
+  bool live;
+  const GemmArgs& g;
+  __device__ __forceinline__ StageIter(const GemmArgs& g_, int cluster, int nclusters, int num_m_blk)
+      : it(g_, cluster, nclusters), nm(num_m_blk), g(g_) {
+    live = it.next(g, w);
+    kb = live ? w.kb0 : 0;
+  }
+  __device__ __forceinline__ int m_blk() const { return w.tile % nm; }
+  __device__ __forceinline__ int n_blk() const { return w.tile / nm; }
+  __device__ __forceinline__ void advance() {
+    if (++kb >= w.kb1) {
+      live = it.next(g, w);
+      kb = live ? w.kb0 : 0;
+    }
+  }
+};
+
 // Ring position: slot index and parity, advanced once per stage.
 struct Ring {
   int idx = 0;
@@ -628,65 +650,78 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(448, 1)
         has_a = (int64_t)m_blk * 2 + rank < a_row_blocks;
         nb = ((int64_t)n_blk * 2 < b_row_blocks) + ((int64_t)n_blk * 2 + 1 < b_row_blocks);
       };
-      auto load_b = [&](int kb, int n_blk, int abi, int sfi) {  // SFB + B of one stage
+      // A stager arrives on full[t % kStages] only after its TMEM SF slot was freed by the MMAs
+      // of stage t - kSfSlots, i.e. after phase t - kStages of that barrier completed.
+      static_assert(C::kSfSlots <= C::kStages, "SF run-ahead must not lap the A/B ring");
+      StageIter sfq(g, cluster, nclusters, num_m_blk);
+      auto issue_next_sf = [&] {
+        if (!sfq.live) return;
+        sm100::mbar_wait(&sf_empty[sf.idx], sf.ph ^ 1);
+        uint32_t nat;
+        bool has_a;
+        int nbk;
+        const int kb = sfq.kb, mb = sfq.m_blk(), nb = sfq.n_blk();
+        sf_bytes(kb, mb, nb, nat, has_a, nbk);
+        sm100::mbar_arrive_expect_tx(&sf_full[sf.idx], (has_a ? nat : 0u) + nat * (uint32_t)nbk);
         const int64_t katom = (int64_t)kb * C::kAtoms;
-        const uint32_t nat = (uint32_t)imin64(C::kAtoms, sf_col_blocks - katom) * 512u;
-        const int64_t rb0 = (int64_t)n_blk * 2;
+        const int64_t ra = (int64_t)mb * 2 + rank, rb0 = (int64_t)nb * 2;
+        if (has_a)
+          sm100::bulk_load(smem + C::kOffSfa + sf.idx * C::kSfaBytes, g.a_sf + (ra * sf_col_blocks + katom) * 512,
+                           nat, &sf_full[sf.idx]);
 #pragma unroll
         for (int j = 0; j < 2; ++j)
           if (rb0 + j < b_row_blocks)
-            sm100::bulk_load(smem + C::kOffSfb + sfi * C::kSfbBytes + j * C::kSfaBytes,
-                             g.b_sf + ((rb0 + j) * sf_col_blocks + katom) * 512, nat, &sf_full[sfi]);
-        tma_load_3d_2sm(smem + C::kOffB + abi * C::kBBytes, &tmB, sm100::leader_bar(&full[abi]),
-                        n_blk * 256 + (int)rank * 128, kb * C::kSlices);
+            sm100::bulk_load(smem + C::kOffSfb + sf.idx * C::kSfbBytes + j * C::kSfaBytes,
+                             g.b_sf + ((rb0 + j) * sf_col_blocks + katom) * 512, nat, &sf_full[sf.idx]);
+        sfq.advance();
+        sf.next<C::kSfSlots>();
       };
-      auto load_a = [&](int kb, int m_blk, int abi, int sfi) {  // SFA + A of one stage
-        const int64_t katom = (int64_t)kb * C::kAtoms;
-        const uint32_t nat = (uint32_t)imin64(C::kAtoms, sf_col_blocks - katom) * 512u;
-        const int64_t ra = (int64_t)m_blk * 2 + rank;
-        if (ra < a_row_blocks)
-          sm100::bulk_load(smem + C::kOffSfa + sfi * C::kSfaBytes, g.a_sf + (ra * sf_col_blocks + katom) * 512, nat,
-                           &sf_full[sfi]);
+      auto load_a_codes = [&](int kb, int m_blk, int abi) {
         tma_load_3d_2sm(smem + C::kOffA + abi * C::kABytes, &tmA, sm100::leader_bar(&full[abi]),
                         m_blk * 256 + (int)rank * 128, kb * C::kSlices);
       };
-      auto arm = [&](int kb, int m_blk, int n_blk, int abi, int sfi) {  // expect all bytes of a stage
-        uint32_t nat;
-        bool has_a;
-        int nb;
-        sf_bytes(kb, m_blk, n_blk, nat, has_a, nb);
-        sm100::mbar_arrive_expect_tx(&sf_full[sfi], (has_a ? nat : 0u) + nat * (uint32_t)nb);
+      auto load_b_codes = [&](int kb, int n_blk, int abi) {
+        tma_load_3d_2sm(smem + C::kOffB + abi * C::kBBytes, &tmB, sm100::leader_bar(&full[abi]),
+                        n_blk * 256 + (int)rank * 128, kb * C::kSlices);
+      };
+      auto arm_ab = [&](int abi) {
         if (leader) sm100::mbar_arrive_expect_tx(&full[abi], 2u * (C::kABytes + C::kBBytes));
       };
-      int pre = 0;  // stages of the first item whose weight half was issued before the PDL wait
+      // Scale factors run one stage ahead of the A/B codes (SF of stage t is issued right after
+      // the A/B of stage t - 1): the peer CTA's scale factors then reach the leader through the
+      // cluster-scope release (forwarder below) before the MMAs of stage t are due.  Measured
+      // (scripts/ahead_probe.py): 1 stage ahead 59.6 us vs 69.1 (none) at c1; more is no faster.
+      constexpr int ahead = 1;
+      int pre = 0;
       if (it.next(g, w)) {
         const int m_blk = w.tile % num_m_blk, n_blk = w.tile / num_m_blk;
-        pre = g.preissue ? min(min(C::kStages, C::kSfSlots), w.kb1 - w.kb0) : 0;
-        for (int s2 = 0; s2 < pre; ++s2) {  // fresh barriers: no empty waits needed
-          arm(w.kb0 + s2, m_blk, n_blk, s2, s2);
-          load_b(w.kb0 + s2, n_blk, s2, s2);
-        }
-        pdl_wait();  // A, its scale factors and tensor scale come from the act-quant kernel
-        for (int s2 = 0; s2 < pre; ++s2) load_a(w.kb0 + s2, m_blk, s2, s2);
+        pre = g.preissue ? min(C::kStages, w.kb1 - w.kb0) : 0;
         for (int s2 = 0; s2 < pre; ++s2) {
+          arm_ab(s2);
+          load_b_codes(w.kb0 + s2, n_blk, s2);
+        }
+        pdl_wait();
+        for (int s2 = 0; s2 < ahead; ++s2) issue_next_sf();
+        for (int s2 = 0; s2 < pre; ++s2) {
+          load_a_codes(w.kb0 + s2, m_blk, s2);
           ab.next<C::kStages>();
-          sf.next<C::kSfSlots>();
+          issue_next_sf();
         }
         bool more = true;
         while (more) {
           const int mb = w.tile % num_m_blk, nb = w.tile / num_m_blk;
           for (int kb = w.kb0 + pre; kb < w.kb1; ++kb) {
-            sm100::mbar_wait(&sf_empty[sf.idx], sf.ph ^ 1);
             sm100::mbar_wait(&empty[ab.idx], ab.ph ^ 1);
-            arm(kb, mb, nb, ab.idx, sf.idx);
-            load_a(kb, mb, ab.idx, sf.idx);
-            load_b(kb, nb, ab.idx, sf.idx);
+            arm_ab(ab.idx);
+            load_a_codes(kb, mb, ab.idx);
+            load_b_codes(kb, nb, ab.idx);
             ab.next<C::kStages>();
-            sf.next<C::kSfSlots>();
+            issue_next_sf();
           }
           pre = 0;
           more = it.next(g, w);
         }
+        while (sfq.live) issue_next_sf();
       } else {
         pdl_wait();
       }
@@ -778,8 +813,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(448, 1)
             rb[8 * a + 4 * j + 2] = vb.z; rb[8 * a + 4 * j + 3] = vb.w;
           }
         }
-        __syncwarp();
-        if (lane == 0) sm100::mbar_arrive(&sf_empty[sf.idx]);   // SMEM slot consumed (values in registers)
         sm100::mbar_wait(&tsf_empty[sf.idx], sf.ph ^ 1);        // TMEM slot's previous MMAs done
         sm100::tc_fence_after();
         const uint32_t t0 = tmem_base + ((uint32_t)(q * 32) << 16) + C::kAccCols + sf.idx * C::kSfCols;
@@ -790,6 +823,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(448, 1)
         sm100::tmem_st_wait();
         sm100::tc_fence_before();
         __syncwarp();
+        // The SMEM slot is released only once its values have been consumed (stored to TMEM):
+        // with the scale factors issued ahead of the A/B codes the producer refills a freed slot
+        // at once, and an arrival right after the 16-B shared loads let that refill race them.
+        if (lane == 0) sm100::mbar_arrive(&sf_empty[sf.idx]);
         if (lane == 0) sm100::mbar_arrive(leader ? &full[ab.idx] : &staged[ab.idx]);
         ab.next<C::kStages>();
         sf.next<C::kSfSlots>();
