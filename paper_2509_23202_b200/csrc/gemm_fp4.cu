@@ -448,7 +448,7 @@ struct Cfg2 {
   static constexpr int kOffBar = kOffSfb + kSfSlots * kSfbBytes;
   static constexpr int kSmem = kOffBar + 512 + 1024;
   static_assert(kSmem <= 232448, "SMEM budget");
-  static constexpr int kThreads2 = 448;
+  static constexpr int kThreads2 = 480;   // + warp 14: second peer-SF forwarder
   static constexpr int kEpiWarps = 8;   // 2 per TMEM lane quadrant, 128 accumulator columns each
 };
 
@@ -586,7 +586,7 @@ struct Ring {
 };
 
 template <int VEC, int OUT, int HKQ = 0>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(448, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(480, 1)
     k_gemm_fp4_2sm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs g) {
   using C = Cfg2<VEC>;
   extern __shared__ uint8_t smem_raw[];
@@ -726,7 +726,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(448, 1)
         pdl_wait();
       }
     }
-  } else if (warp == 1 && !leader) {
+  } else if ((warp == 1 || warp == 14) && !leader) {
     // ------------------------------------------------- peer SF forwarder (non-leader)
     // The leader's MMAs read this CTA's scale factors from this CTA's TMEM.  Ordering those
     // tcgen05.st before the MMAs needs a CLUSTER-scope release: with a cta-scope one the MMAs
@@ -734,14 +734,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(448, 1)
     // 8192 x 16384 -> 53248, tests/test_gpu_fullsize.py).  A cluster-scope release is a
     // MEMBAR.ALL.GPU, so one thread pays it per stage here, off the stager warps' path: it
     // collects the 4 local stager arrivals and forwards one arrival to the leader's `full`.
+    // Two forwarders (warps 1 and 14) take alternate stages, so a slow membar under heavy
+    // memory traffic does not queue the next stage behind it.
     if (lane == 0) {
       Ring ab;
       WorkIter it(g, cluster, nclusters);
       Work w;
+      int st = 0;
+      const int mine = warp == 1 ? 0 : 1;
       while (it.next(g, w)) {
-        for (int kb = w.kb0; kb < w.kb1; ++kb) {
-          sm100::mbar_wait(&staged[ab.idx], ab.ph);
-          sm100::mbar_arrive_remote(&full[ab.idx], 0);
+        for (int kb = w.kb0; kb < w.kb1; ++kb, ++st) {
+          if ((st & 1) == mine) {
+            sm100::mbar_wait(&staged[ab.idx], ab.ph);
+            sm100::mbar_arrive_remote(&full[ab.idx], 0);
+          }
           ab.next<C::kStages>();
         }
       }
@@ -787,6 +793,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(448, 1)
         acc_phase ^= 1;
       }
     }
+  } else if (warp == 14) {
+    // leader CTA: no role for the second forwarder warp
   } else if (warp < 6) {
     // ------------------------------------------ scale-factor stagers (both CTAs)
     // TMEM slot layout (replicated over the 4 lane quadrants, as tcgen05.cp.warpx4
