@@ -167,6 +167,10 @@ int mrfp4_mse_pass(const double* y, int64_t ngroups, int fmt, const double* cand
                    uint8_t* codes, uint32_t* status, void* stream);
 int mrfp4_mse_group_err(const double* y, int64_t ngroups, int fmt, const double* decoded, double ts,
                         double* group_err, uint32_t* status, void* stream);
+/* out[i] = numpy's pairwise sum (np.sum) of a[starts[i] .. starts[i] + lens[i]) -- the segment
+ * sums the MSE driver combines on the host in numpy's order (bit-identical totals). */
+int mrfp4_pairwise_sums(const double* a, const int64_t* starts, const int64_t* lens, int64_t nseg, double* out,
+                        void* stream);
 
 #ifdef __cplusplus
 }

@@ -27,6 +27,8 @@ int launch_gemm_quant_next(const uint8_t* a, const uint8_t* a_sf, const float* a
                            const uint8_t* b_sf, const float* b_ts, void* y, int64_t ldy, int64_t M, int64_t N,
                            int64_t K, int fmt, int next_hk, uint8_t* q_codes, uint8_t* q_sf, float* q_ts,
                            uint32_t* q_status, cudaStream_t s);
+int launch_np_pairwise_segments(const double* a, const int64_t* starts, const int64_t* lens, int64_t nseg,
+                                double* out, cudaStream_t s);
 int launch_mse_pass(const double* y, int64_t ngroups, int fmt, const double* cand, int ncand, const double* raw0,
                     double sg, double ts, uint8_t* sc, double* dec, double* gerr, uint8_t* codes, uint32_t* status,
                     cudaStream_t s);
@@ -224,4 +226,12 @@ int mrfp4_gemm_quant_next(const uint8_t* a, const uint8_t* a_sf, const float* a_
                                                    next_had_k, next_codes, next_sf, next_tensor_scale, status,
                                                    static_cast<cudaStream_t>(stream)),
                      "mrfp4_gemm_quant_next");
+}
+
+int mrfp4_pairwise_sums(const double* a, const int64_t* starts, const int64_t* lens, int64_t nseg, double* out,
+                        void* stream) {
+  if (nseg < 1) return fail(MRFP4_EINVAL, "no segments");
+  if (!a || !starts || !lens || !out) return fail(MRFP4_EINVAL, "null buffer");
+  return cuda_status(mrfp4::launch_np_pairwise_segments(a, starts, lens, nseg, out, static_cast<cudaStream_t>(stream)),
+                     "mrfp4_pairwise_sums");
 }

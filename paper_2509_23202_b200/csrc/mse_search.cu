@@ -150,6 +150,38 @@ __global__ void __launch_bounds__(128) k_mse_group_err(const double* __restrict_
   }
 }
 
+// numpy's pairwise_sum (umath loops: n < 8 sequential from 0; n <= 128 eight accumulators
+// combined as ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) plus the tail; larger n split at
+// n2 = n/2 rounded down to a multiple of 8).  Bit-identical to np.sum of a float64 array.
+__device__ double np_pairwise(const double* a, int64_t n) {
+  if (n < 8) {
+    double r = 0.0;
+    for (int64_t i = 0; i < n; ++i) r += a[i];
+    return r;
+  }
+  if (n <= 128) {
+    double r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = a[j];
+    int64_t i = 8;
+    for (; i < n - (n % 8); i += 8)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) r[j] += a[i + j];
+    double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+    for (; i < n; ++i) res += a[i];
+    return res;
+  }
+  int64_t n2 = n / 2;
+  n2 -= n2 % 8;
+  return np_pairwise(a, n2) + np_pairwise(a + n2, n - n2);
+}
+
+__global__ void k_np_pairwise_segments(const double* __restrict__ a, const int64_t* __restrict__ starts,
+                                       const int64_t* __restrict__ lens, int64_t nseg, double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nseg; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = np_pairwise(a + starts[i], lens[i]);
+}
+
 int grid_for(int64_t n) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -179,6 +211,12 @@ int launch_mse_group_err(const double* y, int64_t ngroups, int fmt, const double
     k_mse_group_err<32><<<grid, 128, 0, s>>>(y, ngroups, dec, ts, gerr, status);
   else
     k_mse_group_err<16><<<grid, 128, 0, s>>>(y, ngroups, dec, ts, gerr, status);
+  return cudaPeekAtLastError() == cudaSuccess ? MRFP4_OK : MRFP4_ECUDA;
+}
+
+int launch_np_pairwise_segments(const double* a, const int64_t* starts, const int64_t* lens, int64_t nseg,
+                                double* out, cudaStream_t s) {
+  k_np_pairwise_segments<<<grid_for(nseg), 128, 0, s>>>(a, starts, lens, nseg, out);
   return cudaPeekAtLastError() == cudaSuccess ? MRFP4_OK : MRFP4_ECUDA;
 }
 

@@ -230,6 +230,56 @@ def rotate_f64(X: torch.Tensor, had_k: int) -> torch.Tensor:
     return torch.matmul(Xd.view(M, K // had_k, had_k), H).mul_(1.0 / float(np.sqrt(had_k))).view(M, K)
 
 
+_SEG_LIMIT = 16384   # numpy-recursion subtrees at most this long are summed on the GPU, one per thread
+
+
+class _NpSum:
+    """np.sum of a device float64 vector, bit-identical: numpy's pairwise recursion
+    (umath pairwise_sum) is cut into subtrees of <= _SEG_LIMIT elements, each summed on the GPU
+    by ``mrfp4_pairwise_sums`` with numpy's own recursion, and the subtree sums are added on
+    the host in numpy's tree order."""
+
+    def __init__(self, segments, device, tree=None):
+        self.segments = segments
+        self.tree = tree
+        self.starts = torch.tensor([a for a, _ in segments], dtype=torch.int64, device=device)
+        self.lens = torch.tensor([b for _, b in segments], dtype=torch.int64, device=device)
+        self.out = torch.empty(len(segments), dtype=torch.float64, device=device)
+
+    @classmethod
+    def whole(cls, n: int, device):
+        leaves = []
+
+        def build(lo, m):
+            if m <= _SEG_LIMIT:
+                leaves.append((lo, m))
+                return len(leaves) - 1
+            m2 = m // 2
+            m2 -= m2 % 8
+            return (build(lo, m2), build(lo + m2, m - m2))
+
+        tree = build(0, n)
+        return cls(leaves, device, tree)
+
+    @classmethod
+    def chunks(cls, n: int, chunk: int, device):
+        return cls([(lo, min(chunk, n - lo)) for lo in range(0, n, chunk)], device)
+
+    def segment_sums(self, a: torch.Tensor) -> np.ndarray:
+        _lib.check(_lib.lib().mrfp4_pairwise_sums(_lib.ptr(a), _lib.ptr(self.starts), _lib.ptr(self.lens),
+                                                  len(self.segments), _lib.ptr(self.out),
+                                                  _lib.stream_ptr(torch, a.device)))
+        return self.out.cpu().numpy()
+
+    def total(self, a: torch.Tensor) -> float:
+        sums = self.segment_sums(a)
+
+        def ev(node):
+            return float(sums[node]) if isinstance(node, int) else ev(node[0]) + ev(node[1])
+
+        return ev(self.tree)
+
+
 def mse_optimize_scales(X, spec, transform=None, policy=None) -> GpuQuantResult:
     """``quantize_rtn`` with MSE-optimised scales on the GPU (quantizers.py:330-337,
     ``optimize_group_scales`` :263-327).
@@ -279,20 +329,22 @@ def mse_optimize_scales(X, spec, transform=None, policy=None) -> GpuQuantResult:
     scratch = torch.zeros(12, dtype=torch.int32, device=dev)
     status = _lib.ptr(scratch)
 
+    chunk_sum = _NpSum.chunks(ng, _CHUNK_GROUPS, dev)
+    whole_sum = _NpSum.whole(ng, dev)
+
     def pass_groups(sg: float) -> float:
         ts = float(np.float32(sg * factor))
         _lib.check(L.mrfp4_mse_pass(_lib.ptr(Y), ng, fmt, _lib.ptr(cand), len(cand_np), _lib.ptr(raw0), sg, ts,
                                     _lib.ptr(sc), _lib.ptr(dec), _lib.ptr(gerr), _lib.ptr(codes), status, stream))
-        errs = gerr.cpu().numpy()
-        total = 0.0
-        for lo in range(0, ng, _CHUNK_GROUPS):
-            total += float(errs[lo:lo + _CHUNK_GROUPS].sum())
+        total = 0.0   # quantizers.py:292-301: float(errs[lo:hi].sum()) accumulated chunk by chunk
+        for v in chunk_sum.segment_sums(gerr):
+            total += float(v)
         return total
 
     def total_err(sg: float) -> float:
         ts = float(np.float32(sg * factor))
         _lib.check(L.mrfp4_mse_group_err(_lib.ptr(Y), ng, fmt, _lib.ptr(dec), ts, _lib.ptr(gerr2), status, stream))
-        return float(gerr2.cpu().numpy().sum())
+        return whole_sum.total(gerr2)
 
     best_total = pass_groups(s_global)
     for _ in range(MSE_SEARCH_ROUNDS):

@@ -90,3 +90,15 @@ def test_mse_weight_feeds_the_linear():
                        t.tensor_scale, 0.0, 0.0)
     ref = O.linear_reference(O.quantize_rtn(X, "nvfp4", hadamard=16), Wo)
     assert float(np.linalg.norm(y - ref) / np.linalg.norm(ref)) <= 1e-5
+
+
+@pytest.mark.parametrize("n", [1, 7, 8, 100, 128, 129, 2048, 16384, 16385, 100003, 1 << 20])
+def test_gpu_pairwise_sum_is_numpy_sum(n):
+    """The MSE driver's device sums reproduce np.sum bit for bit (numpy's pairwise recursion)."""
+    from paper_2509_23202_b200.quantize import _NpSum
+    rng = np.random.default_rng(n)
+    a = rng.standard_normal(n) ** 2 * 10.0 ** rng.integers(-8, 8, n)
+    t = torch.from_numpy(a).cuda()
+    assert _NpSum.whole(n, "cuda").total(t) == float(np.sum(a))
+    ch = _NpSum.chunks(n, 2048, "cuda").segment_sums(t)
+    assert all(float(c) == float(np.sum(a[i * 2048:(i + 1) * 2048])) for i, c in enumerate(ch))
