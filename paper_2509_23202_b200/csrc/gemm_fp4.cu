@@ -599,7 +599,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(480, 1)
   uint64_t* tfull = tsf_empty + C::kSfSlots;
   uint64_t* tempty = tfull + 1;
   uint64_t* staged = tempty + 1;                                     // non-leader: its 4 stagers done
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(staged + C::kStages);
+  // NVFP4 hands its scale factors over in two halves (atoms 0-3 for MMAs 0-3, atoms 4-7 for
+  // MMAs 4-7), so the first half can be staged -- and the peer's forwarded -- half a stage
+  // earlier: only 2 TMEM SF slots fit next to the accumulator, and the ~400 ns cluster-scope
+  // release of the peer's handoff otherwise does not fit the one-stage window.
+  constexpr bool kSplit = VEC == 16;
+  uint64_t* staged_b = staged + C::kStages;                          // non-leader: second halves staged
+  uint64_t* sfb_ready = staged_b + C::kStages;                       // leader: second halves staged (both CTAs)
+  uint64_t* tsf_half = sfb_ready + C::kStages;                       // TMEM SF slot's first half free
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tsf_half + C::kSfSlots);
 
   const uint32_t rank = sm100::cluster_ctarank();
   const bool leader = rank == 0;
@@ -617,11 +625,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(480, 1)
       sm100::mbar_init(&full[s], 6);
       sm100::mbar_init(&staged[s], 4);
       sm100::mbar_init(&empty[s], 1);
+      sm100::mbar_init(&staged_b[s], 4);
+      sm100::mbar_init(&sfb_ready[s], 5);   // the leader's 4 stager warps + the peer's forwarder
     }
     for (int s = 0; s < C::kSfSlots; ++s) {
       sm100::mbar_init(&sf_full[s], 1);
       sm100::mbar_init(&sf_empty[s], 4);  // this CTA's 4 stager warps
       sm100::mbar_init(&tsf_empty[s], 1);
+      sm100::mbar_init(&tsf_half[s], 1);
     }
     sm100::mbar_init(tfull, 1);
     sm100::mbar_init(tempty, 2 * C::kEpiWarps);  // epilogue warps x 2 CTAs
@@ -741,13 +752,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(480, 1)
       WorkIter it(g, cluster, nclusters);
       Work w;
       int st = 0;
-      // MXFP4 measured faster with two forwarders (c2-down 200 -> 188 us); NVFP4, bound by its
-      // 2-slot TMEM window rather than by the forwarder, keeps one.
-      constexpr int kFwd = VEC == 32 ? 2 : 1;
+      // MXFP4: the two forwarders take alternate stages (c2-down 200 -> 188 us).  NVFP4: warp 1
+      // forwards every stage's first half, warp 14 every second half.
       const int mine = warp == 1 ? 0 : 1;
       while (it.next(g, w)) {
         for (int kb = w.kb0; kb < w.kb1; ++kb, ++st) {
-          if (st % kFwd == mine) {
+          if constexpr (kSplit) {
+            if (mine == 0) {
+              sm100::mbar_wait(&staged[ab.idx], ab.ph);
+              sm100::mbar_arrive_remote(&full[ab.idx], 0);
+            } else {
+              sm100::mbar_wait(&staged_b[ab.idx], ab.ph);
+              sm100::mbar_arrive_remote(&sfb_ready[ab.idx], 0);
+            }
+          } else if ((st & 1) == mine) {
             sm100::mbar_wait(&staged[ab.idx], ab.ph);
             sm100::mbar_arrive_remote(&full[ab.idx], 0);
           }
@@ -782,10 +800,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(480, 1)
           const uint32_t sfa_t = sf0 + sf.idx * C::kSfCols, sfb_t = sfa_t + C::kSfaCols;
           const uint64_t ad = desc_add(adesc0, (uint32_t)(ab.idx * (C::kABytes >> 4)));
           const uint64_t bd = desc_add(bdesc0, (uint32_t)(ab.idx * (C::kBBytes >> 4)));
-          if (kb + 1 < num_kb || tail_mmas == 0)
-            issue_stage_mmas<VEC, 0, C::kMmas>(el, tmem_base, ad, bd, sfa_t, sfb_t, kb == w.kb0);
-          else
-            issue_stage_tail<VEC>(tail_mmas, el, tmem_base, ad, bd, sfa_t, sfb_t, kb == w.kb0);
+          if constexpr (kSplit) {
+            const int nk = (kb + 1 < num_kb || tail_mmas == 0) ? C::kMmas : tail_mmas;
+            if (nk >= 4) issue_stage_mmas<VEC, 0, 4>(el, tmem_base, ad, bd, sfa_t, sfb_t, kb == w.kb0);
+            else issue_stage_tail<VEC>(nk, el, tmem_base, ad, bd, sfa_t, sfb_t, kb == w.kb0);
+            sm100::tc_commit_2sm_mc_if(el, &tsf_half[sf.idx], 0x3);
+            sm100::mbar_wait(&sfb_ready[ab.idx], ab.ph);   // second halves of both CTAs staged
+            sm100::tc_fence_after();
+            switch (nk) {
+              case 5: issue_stage_mmas<VEC, 4, 5>(el, tmem_base, ad, bd, sfa_t, sfb_t, false); break;
+              case 6: issue_stage_mmas<VEC, 4, 6>(el, tmem_base, ad, bd, sfa_t, sfb_t, false); break;
+              case 7: issue_stage_mmas<VEC, 4, 7>(el, tmem_base, ad, bd, sfa_t, sfb_t, false); break;
+              case 8: issue_stage_mmas<VEC, 4, 8>(el, tmem_base, ad, bd, sfa_t, sfb_t, false); break;
+              default: break;
+            }
+          } else {
+            if (kb + 1 < num_kb || tail_mmas == 0)
+              issue_stage_mmas<VEC, 0, C::kMmas>(el, tmem_base, ad, bd, sfa_t, sfb_t, kb == w.kb0);
+            else
+              issue_stage_tail<VEC>(tail_mmas, el, tmem_base, ad, bd, sfa_t, sfb_t, kb == w.kb0);
+          }
           sm100::tc_commit_2sm_mc_if(el, &empty[ab.idx], 0x3);
           sm100::tc_commit_2sm_mc_if(el, &tsf_empty[sf.idx], 0x3);
           if (dbg && ntl < 4 && kb - w.kb0 < 128) dbg[ntl * 260 + 3 + 2 * (kb - w.kb0)] = clock64();
@@ -824,9 +858,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(480, 1)
             rb[8 * a + 4 * j + 2] = vb.z; rb[8 * a + 4 * j + 3] = vb.w;
           }
         }
+        const uint32_t t0 = tmem_base + ((uint32_t)(q * 32) << 16) + C::kAccCols + sf.idx * C::kSfCols;
+        if constexpr (kSplit) {
+          // first half: SFA columns [0, 16) and SFB columns [0, 32) (atoms 0-3, MMAs 0-3)
+          sm100::mbar_wait(&tsf_half[sf.idx], sf.ph ^ 1);        // previous use's MMAs 0-3 done
+          sm100::tc_fence_after();
+          sm100::tmem_st_32x32b<16>(t0, ra);
+          sm100::tmem_st_32x32b<16>(t0 + C::kSfaCols, rb);
+          sm100::tmem_st_32x32b<16>(t0 + C::kSfaCols + 16, rb + 16);
+          sm100::tmem_st_wait();
+          sm100::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) sm100::mbar_arrive(leader ? &full[ab.idx] : &staged[ab.idx]);
+          sm100::mbar_wait(&tsf_empty[sf.idx], sf.ph ^ 1);       // previous use's MMAs 4-7 done
+          sm100::tc_fence_after();
+          sm100::tmem_st_32x32b<16>(t0 + 16, ra + 16);
+          sm100::tmem_st_32x32b<16>(t0 + C::kSfaCols + 32, rb + 32);
+          sm100::tmem_st_32x32b<16>(t0 + C::kSfaCols + 48, rb + 48);
+          sm100::tmem_st_wait();
+          sm100::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) sm100::mbar_arrive(&sf_empty[sf.idx]);
+          if (lane == 0) sm100::mbar_arrive(leader ? &sfb_ready[ab.idx] : &staged_b[ab.idx]);
+          ab.next<C::kStages>();
+          sf.next<C::kSfSlots>();
+          continue;
+        }
         sm100::mbar_wait(&tsf_empty[sf.idx], sf.ph ^ 1);        // TMEM slot's previous MMAs done
         sm100::tc_fence_after();
-        const uint32_t t0 = tmem_base + ((uint32_t)(q * 32) << 16) + C::kAccCols + sf.idx * C::kSfCols;
 #pragma unroll
         for (int c = 0; c < C::kSfaCols; c += 16) sm100::tmem_st_32x32b<16>(t0 + c, ra + c);
 #pragma unroll
