@@ -69,12 +69,21 @@ class ClockSampler:
         self.proc = None
         self.path = tempfile.mktemp(suffix=".csv")
 
-    def start(self):
+    def start(self, keep_busy=None):
+        """Start sampling and return once the first sample is in (nvidia-smi takes ~0.1-0.5 s to
+        come up; a timed region shorter than that would otherwise see no sample).  keep_busy()
+        is called meanwhile so the GPU stays under the benchmark's load."""
         try:
             self.fh = open(self.path, "w")
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "20",
                  "-i", str(self.dev)], stdout=self.fh, stderr=subprocess.DEVNULL)
+            t0 = time.time()
+            while time.time() - t0 < 5.0 and os.path.getsize(self.path) == 0:
+                if keep_busy is not None:
+                    keep_busy()
+                else:
+                    time.sleep(0.01)
         except Exception:
             self.proc = None
         return self
@@ -231,7 +240,15 @@ def main():
     for _ in range(args.warmup):
         flush_l2()
         step()
-    sampler = ClockSampler(torch.cuda.current_device()).start()
+    def busy():   # local work only (no collective: ranks may loop a different number of times)
+        for _ in range(10):
+            flush_l2()
+            act_quant_into(x, w.fmt, had, a.codes, a.sf, a.tensor_scale_dev, a.scratch)
+            P.gemm(a, w, y)
+        torch.cuda.synchronize(dev)
+
+    # sampling runs from just before the timed region (under the same load) to its end
+    sampler = ClockSampler(torch.cuda.current_device()).start(keep_busy=busy)
     barrier()
     ev_step = timed(step, args.steps)              # the timed region: exactly K steps
     barrier()
