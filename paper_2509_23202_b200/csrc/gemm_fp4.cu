@@ -698,11 +698,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(480, 1)
       auto arm_ab = [&](int abi) {
         if (leader) sm100::mbar_arrive_expect_tx(&full[abi], 2u * (C::kABytes + C::kBBytes));
       };
-      // Scale factors run one stage ahead of the A/B codes (SF of stage t is issued right after
-      // the A/B of stage t - 1): the peer CTA's scale factors then reach the leader through the
-      // cluster-scope release (forwarder below) before the MMAs of stage t are due.  Measured
-      // (scripts/ahead_probe.py): 1 stage ahead 59.6 us vs 69.1 (none) at c1; more is no faster.
-      constexpr int ahead = 1;
+      // Scale factors run ahead of the A/B codes (SF of stage t is issued right after the A/B of
+      // stage t - ahead): the peer CTA's scale factors then reach the leader through the
+      // cluster-scope release (forwarder below) before the MMAs of stage t are due
+      // (scripts/ahead_probe.py).
+      // MXFP4 (3 SF slots, 2 forwarders) runs two stages ahead: c1 56.1 -> 53.4 us, 70B down
+      // 191.7 -> 180.5; NVFP4 (2 slots) is best at one (223.8 vs 229.7 at two).
+      constexpr int ahead = VEC == 32 ? 2 : 1;
       int pre = 0;
       if (it.next(g, w)) {
         const int m_blk = w.tile % num_m_blk, n_blk = w.tile / num_m_blk;
