@@ -133,6 +133,18 @@ int mrfp4_dequantize(const uint8_t* codes, const uint8_t* sf, const float* tenso
                      int64_t rows, int64_t cols, int fmt, float* out, void* stream);
 
 /*
+ * K2 of an N-sharded linear with the output all-gather fused into its epilogue (SURVEY.md
+ * 8(f) row f1): D = a . b^T (bf16) stored row segment by row segment into EACH of the ndst
+ * (<= 8) destinations -- on a multi-GPU node, the peer-mapped full-output buffers of every rank
+ * (e.g. torch symmetric memory over NVLink), each pointer already offset to this rank's column
+ * block; row stride ldd (the full N).  Replaces mrfp4_gemm + the NCCL all-gather of the bf16
+ * output.  The caller synchronizes the ranks afterwards.  Requires M > 128, K % 256 == 0.
+ */
+int mrfp4_gemm_peers(const uint8_t* a, const uint8_t* a_sf, const float* a_ts, const uint8_t* b, const uint8_t* b_sf,
+                     const float* b_ts, void* const* dsts, int ndst, int64_t M, int64_t N, int64_t K, int64_t ldd,
+                     int fmt, void* stream);
+
+/*
  * K2 with the NEXT layer's act-quant fused into its epilogue: computes
  * Y = bf16(a . b^T) as mrfp4_gemm does and, from those bf16 values, the MXFP4 quantization
  * quantize_rtn(Y, FormatSpec.mxfp4(), transform=hadamard(next_had_k)) (quantizers.py:247-255)

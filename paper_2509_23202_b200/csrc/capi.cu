@@ -27,6 +27,9 @@ int launch_gemm_quant_next(const uint8_t* a, const uint8_t* a_sf, const float* a
                            const uint8_t* b_sf, const float* b_ts, void* y, int64_t ldy, int64_t M, int64_t N,
                            int64_t K, int fmt, int next_hk, uint8_t* q_codes, uint8_t* q_sf, float* q_ts,
                            uint32_t* q_status, cudaStream_t s);
+int launch_gemm_peers(const uint8_t* a, const uint8_t* a_sf, const float* a_ts, const uint8_t* b,
+                      const uint8_t* b_sf, const float* b_ts, void* const* dsts, int ndst, int64_t M, int64_t N,
+                      int64_t K, int64_t ldd, int fmt, cudaStream_t s);
 int launch_np_pairwise_segments(const double* a, const int64_t* starts, const int64_t* lens, int64_t nseg,
                                 double* out, cudaStream_t s);
 int launch_mse_pass(const double* y, int64_t ngroups, int fmt, const double* cand, int ncand, const double* raw0,
@@ -234,4 +237,22 @@ int mrfp4_pairwise_sums(const double* a, const int64_t* starts, const int64_t* l
   if (!a || !starts || !lens || !out) return fail(MRFP4_EINVAL, "null buffer");
   return cuda_status(mrfp4::launch_np_pairwise_segments(a, starts, lens, nseg, out, static_cast<cudaStream_t>(stream)),
                      "mrfp4_pairwise_sums");
+}
+
+int mrfp4_gemm_peers(const uint8_t* a, const uint8_t* a_sf, const float* a_ts, const uint8_t* b, const uint8_t* b_sf,
+                     const float* b_ts, void* const* dsts, int ndst, int64_t M, int64_t N, int64_t K, int64_t ldd,
+                     int fmt, void* stream) {
+  if (mrfp4_group_size(fmt) == 0) return fail(MRFP4_EUNSUPPORTED, "unknown format %d", fmt);
+  if (M < 1 || N < 1 || K < 1) return fail(MRFP4_EINVAL, "empty GEMM");
+  if (M <= 128 || K % 256)
+    return fail(MRFP4_EUNSUPPORTED, "peer-store GEMM needs M > 128 and K %% 256 == 0 (2-CTA GEMM)");
+  if (N % 8) return fail(MRFP4_EUNSUPPORTED, "N (%lld) must be a multiple of 8", (long long)N);
+  if (ndst < 1 || ndst > 8 || !dsts) return fail(MRFP4_EINVAL, "1..8 destinations");
+  if (ldd < N || ldd % 16) return fail(MRFP4_EINVAL, "ldd must be >= N and a multiple of 16");
+  for (int i = 0; i < ndst; ++i)
+    if (!dsts[i] || !aligned(dsts[i], 32)) return fail(MRFP4_EINVAL, "destinations must be 32-byte aligned");
+  if (!a || !a_sf || !a_ts || !b || !b_sf || !b_ts) return fail(MRFP4_EINVAL, "null buffer");
+  return cuda_status(mrfp4::launch_gemm_peers(a, a_sf, a_ts, b, b_sf, b_ts, dsts, ndst, M, N, K, ldd, fmt,
+                                              static_cast<cudaStream_t>(stream)),
+                     "mrfp4_gemm_peers");
 }

@@ -92,6 +92,11 @@ struct GemmArgs {
   uint32_t q_cb;      // scale column blocks of the next layer: N / 32 / 4
   int64_t q_rows_pad; // ceil(M / 128) * 128
   qc::AQParams qp;    // c64 / kraw / kmx / pm of the next layer's rotation
+  // Fused output all-gather (SURVEY.md 8(f) row f1, 2-CTA kernel, bf16): every output row
+  // segment is stored to each of npeer destinations (peer-mapped over NVLink on a multi-GPU
+  // node; each already offset to this rank's column block of that rank's full output).
+  int npeer;
+  void* peer_d[8];
 };
 constexpr int kOutMxq = 100;  // internal OUT tag (not an ABI dtype)
 
@@ -953,17 +958,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(480, 1)
           if (!g.d) continue;
         }
         if (row < g.M) {
-          __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(g.d) + row * g.ldd + col0;
-          // 32-B stores: whole L2 sectors per lane (16-B stores from 32 rows at once were
-          // partial-sector writes that stalled the next tile's pipeline by ~5K cycles).
-          if ((g.ldd & 15) == 0 && col0 + 128 <= g.N) {
+          const int nd = g.npeer > 0 ? g.npeer : 1;
+#pragma unroll 1
+          for (int pd = 0; pd < nd; ++pd) {
+            __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(g.npeer > 0 ? g.peer_d[pd] : g.d) + row * g.ldd + col0;
+            // 32-B stores: whole L2 sectors per lane (16-B stores from 32 rows at once were
+            // partial-sector writes that stalled the next tile's pipeline by ~5K cycles).
+            if ((g.ldd & 15) == 0 && col0 + 128 <= g.N) {
 #pragma unroll
-            for (int j = 0; j < 8; ++j) st_global_v8(dst + 16 * j, pkd + 8 * j);
-          } else {
+              for (int j = 0; j < 8; ++j) st_global_v8(dst + 16 * j, pkd + 8 * j);
+            } else {
 #pragma unroll
-            for (int j = 0; j < 16; ++j)
-              if (col0 + 8 * j < g.N)
-                *reinterpret_cast<uint4*>(dst + 8 * j) = make_uint4(pkd[4 * j], pkd[4 * j + 1], pkd[4 * j + 2], pkd[4 * j + 3]);
+              for (int j = 0; j < 16; ++j)
+                if (col0 + 8 * j < g.N)
+                  *reinterpret_cast<uint4*>(dst + 8 * j) = make_uint4(pkd[4 * j], pkd[4 * j + 1], pkd[4 * j + 2], pkd[4 * j + 3]);
+            }
           }
         }
       } else {
@@ -1188,6 +1197,28 @@ int launch_gemm_fp4(const uint8_t* a, const uint8_t* a_sf, const float* a_ts, co
   }
   return d_dtype == MRFP4_DT_BF16 ? launch<32, 256, MRFP4_DT_BF16>(a, b, g, s)
                                   : launch<32, 256, MRFP4_DT_F32>(a, b, g, s);
+}
+
+// K2 storing its bf16 output straight into several (peer) output buffers: the all-gather
+// of the N-sharded linear fused into the epilogue (2-CTA kernel only).
+int launch_gemm_peers(const uint8_t* a, const uint8_t* a_sf, const float* a_ts, const uint8_t* b,
+                      const uint8_t* b_sf, const float* b_ts, void* const* dsts, int ndst, int64_t M, int64_t N,
+                      int64_t K, int64_t ldd, int fmt, cudaStream_t s) {
+  GemmArgs g{};
+  g.b = b;
+  g.preissue = g_preissue;
+  g.a_sf = a_sf;
+  g.b_sf = b_sf;
+  g.a_ts = a_ts;
+  g.b_ts = b_ts;
+  g.d = dsts[0];
+  g.M = M;
+  g.N = N;
+  g.K = K;
+  g.ldd = ldd;
+  g.npeer = ndst;
+  for (int i = 0; i < ndst; ++i) g.peer_d[i] = dsts[i];
+  return fmt == MRFP4_FMT_NVFP4 ? launch2<16, MRFP4_DT_BF16>(a, b, g, s) : launch2<32, MRFP4_DT_BF16>(a, b, g, s);
 }
 
 // K2 with the next layer's MXFP4 act-quant fused into the epilogue (2-CTA kernel only).

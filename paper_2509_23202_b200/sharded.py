@@ -37,11 +37,50 @@ def gather_columns(y_shard: torch.Tensor, group=None) -> torch.Tensor:
 
 
 def quantized_linear_sharded(x: torch.Tensor, w_shard: PackedWeight, group=None, *,
-                             out_dtype=torch.bfloat16, gather: bool = True) -> torch.Tensor:
-    """Per-rank K1 + K2 on the weight shard, then NCCL all-gather of the output."""
+                             out_dtype=torch.bfloat16, gather: bool = True, peer_outputs=None) -> torch.Tensor:
+    """Per-rank K1 + K2 on the weight shard, then NCCL all-gather of the output.
+
+    ``peer_outputs``: every rank's full [M, N] bf16 output buffer mapped into this process
+    (symmetric memory over NVLink), indexed by rank.  K2 then stores this rank's columns into all
+    of them from its epilogue (``gemm_into_peers``) instead of running the NCCL all-gather; the
+    ranks synchronize before the result is returned.  (Emulation-tested on one GPU only.)"""
+    if peer_outputs is not None:
+        from .quantize import act_quant_into, alloc_result, as_device_matrix
+        rank = dist.get_rank(group)
+        x2 = as_device_matrix(x.reshape(-1, x.shape[-1]), w_shard.device)
+        a = alloc_result(x2.shape[0], x2.shape[1], w_shard.fmt, w_shard.had_k, x2.device)
+        act_quant_into(x2, w_shard.fmt, w_shard.had_k, a.codes, a.sf, a.tensor_scale_dev, a.scratch)
+        n = w_shard.N
+        gemm_into_peers(a, w_shard, [po[:, rank * n:(rank + 1) * n] for po in peer_outputs])
+        torch.cuda.current_stream(x2.device).synchronize()
+        dist.barrier(group)
+        return peer_outputs[rank]
     y = quantized_linear(x, w_shard, out_dtype=out_dtype)
     y2 = y.reshape(-1, w_shard.N)
     if not gather:
         return y
     full = gather_columns(y2, group)
     return full.reshape(*x.shape[:-1], full.shape[-1])
+
+
+def gemm_into_peers(a, w_shard: PackedWeight, outs: list) -> None:
+    """K2 of this rank's weight shard with the output all-gather fused into the epilogue
+    (``mrfp4_gemm_peers``): every output row segment is stored into each
+    tensor of ``outs`` -- this rank's [M, N/P] column block inside every rank's full [M, N]
+    bf16 output, peer-mapped (e.g. ``torch.distributed._symmetric_memory`` buffers over
+    NVLink) or local.  The caller synchronizes the ranks before reading."""
+    import ctypes
+
+    from . import _lib
+    if not 1 <= len(outs) <= 8:
+        raise DataError("1..8 destinations")
+    M = a.rows
+    ldd = outs[0].stride(0)
+    for o in outs:
+        if o.dtype != torch.bfloat16 or tuple(o.shape) != (M, w_shard.N) or o.stride() != (ldd, 1):
+            raise DataError("destinations must be bf16 [M, N/P] views with one common row stride")
+    arr = (ctypes.c_void_p * len(outs))(*[o.data_ptr() for o in outs])
+    _lib.check(_lib.lib().mrfp4_gemm_peers(
+        _lib.ptr(a.codes), _lib.ptr(a.sf), _lib.ptr(a.tensor_scale_dev),
+        _lib.ptr(w_shard.codes), _lib.ptr(w_shard.sf), _lib.ptr(w_shard.tensor_scale_dev),
+        arr, len(outs), M, w_shard.N, w_shard.K, ldd, w_shard.fmt, _lib.stream_ptr(torch, outs[0].device)))

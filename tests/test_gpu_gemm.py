@@ -243,3 +243,28 @@ def test_graphed_linear_matches_eager(fmt, k, M):
         y = g(X).clone()
         torch.cuda.synchronize()
         assert torch.equal(y, P.quantized_linear(X, w))
+
+
+@pytest.mark.parametrize("fmt,M", [("mxfp4", 512), ("nvfp4", 300)])
+def test_fused_gather_peer_stores_emulated(fmt, M):
+    """The all-gather fused into K2's epilogue (mrfp4_gemm_peers), emulated on one GPU: 4 ranks'
+    output buffers are local tensors; each rank's shard GEMM stores its column block into all
+    four.  Every buffer must equal the unsharded linear, bit for bit."""
+    from paper_2509_23202_b200.quantize import act_quant_into, alloc_result
+    from paper_2509_23202_b200.sharded import gemm_into_peers
+    P_, K, N = 4, 1024, 2048
+    rng = np.random.default_rng(M)
+    X = torch.from_numpy(O.bf16_round(rng.standard_normal((M, K)))).cuda().bfloat16()
+    W = torch.from_numpy(O.bf16_round(rng.standard_normal((N, K)) / 32)).cuda().bfloat16()
+    k = 32 if fmt == "mxfp4" else 16
+    w = P.quantize_weight(W, SPEC[fmt], P.TransformSpec.hadamard(k))
+    ref = P.quantized_linear(X, w)
+    a = alloc_result(M, K, w.fmt, k, "cuda")
+    act_quant_into(X, w.fmt, k, a.codes, a.sf, a.tensor_scale_dev, a.scratch)
+    bufs = [torch.full((M, N), float("nan"), dtype=torch.bfloat16, device="cuda") for _ in range(P_)]
+    n = N // P_
+    for r in range(P_):
+        gemm_into_peers(a, w.shard(r, P_), [b[:, r * n:(r + 1) * n] for b in bufs])
+    torch.cuda.synchronize()
+    for b in bufs:
+        assert torch.equal(b, ref)
