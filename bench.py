@@ -211,9 +211,8 @@ def main():
         flush_w.zero_()                    # write a buffer larger than L2 (126 MB) ...
         flush_r.sum(dtype=torch.int32)     # ... then read another: L2 left clean, none of our data
 
-    # K1 (one launch for both formats) + K2 (+ the split-K reduce for small M)
-    from paper_2509_23202_b200 import _lib
-    launches_per_step = 2 + (1 if _lib.lib().mrfp4_gemm_workspace(M, w.N, K, w.fmt) > 0 else 0)
+    # K1 (one launch for both formats) + K2 (split-K for small M reduces inside K2)
+    launches_per_step = 2
 
     def step():
         act_quant_into(x, w.fmt, had, a.codes, a.sf, a.tensor_scale_dev, a.scratch)

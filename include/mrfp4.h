@@ -116,11 +116,10 @@ int mrfp4_sf_unswizzle(const uint8_t* sf_swizzled, uint8_t* sf_rowmajor,
  * a_ts, b_ts: device float tensor scales; d: [M, N] row stride ldd, dtype d_dtype
  * (MRFP4_DT_BF16 or MRFP4_DT_F32).  Requires K % 64 == 0, N % 8 == 0.
  * workspace: device scratch of mrfp4_gemm_workspace() bytes, zero-filled once before first
- * use (every call leaves its flag words zero again; do not share one workspace between
- * concurrent streams).  Small M: split-K fp32 partials reduced in a fixed order by a second
- * kernel.  Large M: the stream-K tail of the 2-CTA kernel (the last tiles' k-stages spread
- * over all SM pairs, fp32 partials reduced in a fixed order).  NULL or too small: neither
- * (correct, slower).
+ * use (a 4 KB header of per-tile arrival counters that every call leaves zero again; do not
+ * share one workspace between concurrent streams).  Small M: split-K fp32 partials, summed in
+ * split order by the last split of each tile to finish (one kernel, deterministic).  Large M:
+ * no workspace (0 bytes).  NULL or too small: no split (correct, slower).
  */
 size_t mrfp4_gemm_workspace(int64_t M, int64_t N, int64_t K, int fmt);
 int mrfp4_gemm(const uint8_t* a, const uint8_t* a_sf, const float* a_ts,

@@ -97,7 +97,12 @@ struct GemmArgs {
   // node; each already offset to this rank's column block of that rank's full output).
   int npeer;
   void* peer_d[8];
+  // 1-CTA split-K: per-tile arrival counters (zero between calls); the last split of a tile to
+  // finish sums all splits' partials in split order (deterministic) and writes the output,
+  // replacing the separate reduce kernel.  Null: the reduce kernel runs.
+  uint32_t* sk_cnt;
 };
+constexpr size_t kSplitkHeader = 4096;   // counters, ahead of the fp32 partials in the workspace
 constexpr int kOutMxq = 100;  // internal OUT tag (not an ABI dtype)
 
 // Swizzled scale-factor offset (128 x 4 atoms), 32-bit.
@@ -370,6 +375,60 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) sm100::mbar_arrive(tempty);
       acc_phase ^= 1;
+      if (g.splits > 1 && g.sk_cnt) {
+        // ---- in-kernel split-K reduction.  Every unit is resident at once (units <= SMs, one
+        // CTA each, checked by the host), so the tile's splits wait for each other and then each
+        // reduces 1/splits of the tile, summing ALL splits' partials in split order (the same
+        // order, hence the same bits, as a separate reduce kernel).  Counter pair per tile:
+        // [0] partials written, [1] slices reduced; the last slice re-arms both.
+        uint32_t* cnt = g.sk_cnt + 2 * tile;
+        const int et = threadIdx.x - 64;   // epilogue thread 0..127 (warps 2-5)
+        __threadfence();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (et == 0) {
+          atomicAdd(cnt, 1u);
+          uint32_t seen;
+          do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(cnt) : "memory");
+          } while (seen < (uint32_t)g.splits);
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        __threadfence();
+        const int64_t r0 = (int64_t)m_blk * BM, c0 = (int64_t)n_blk * BN;
+        const int rows = (int)imin64(BM, g.M - r0), c4 = (int)imin64(BN, g.N - c0) / 4;
+        const int total = rows * c4, chunk = (total + g.splits - 1) / g.splits;
+        const int e_end = min(total, (split + 1) * chunk);
+        for (int e = split * chunk + et; e < e_end; e += 128) {
+          const int rr = e / c4, cc = (e - rr * c4) * 4;
+          const int64_t off = (r0 + rr) * g.N + c0 + cc;
+          float4 acc = make_float4(-0.f, -0.f, -0.f, -0.f);   // -0 + x == x bit for bit
+          for (int s0 = 0; s0 < g.splits; s0 += 8) {
+            float4 v[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              if (s0 + j < g.splits) v[j] = __ldcg(reinterpret_cast<const float4*>(g.ws + (int64_t)(s0 + j) * g.M * g.N + off));
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              if (s0 + j < g.splits) { acc.x += v[j].x; acc.y += v[j].y; acc.z += v[j].z; acc.w += v[j].w; }
+          }
+          if constexpr (OUT == MRFP4_DT_BF16) {
+            __nv_bfloat162 lo = __floats2bfloat162_rn(acc.x * alpha, acc.y * alpha);
+            __nv_bfloat162 hi = __floats2bfloat162_rn(acc.z * alpha, acc.w * alpha);
+            uint2 pk;
+            pk.x = *reinterpret_cast<uint32_t*>(&lo);
+            pk.y = *reinterpret_cast<uint32_t*>(&hi);
+            *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(g.d) + (r0 + rr) * g.ldd + c0 + cc) = pk;
+          } else {
+            *reinterpret_cast<float4*>(static_cast<float*>(g.d) + (r0 + rr) * g.ldd + c0 + cc) =
+                make_float4(acc.x * alpha, acc.y * alpha, acc.z * alpha, acc.w * alpha);
+          }
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (et == 0 && atomicAdd(cnt + 1, 1u) == (uint32_t)g.splits - 1) {
+          cnt[0] = 0u;   // every split has passed its wait: re-arm for the next call
+          cnt[1] = 0u;
+        }
+      }
     }
   }
   __syncthreads();
@@ -379,33 +438,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-
-// Split-K reduction: d[m, n] = ts_A * ts_W * sum_s ws[s][m][n] (fixed order: deterministic).
-template <int OUT>
-__global__ void __launch_bounds__(256) k_splitk_reduce(const float* __restrict__ ws, int splits, const float* a_ts,
-                                                       const float* b_ts, void* d, int64_t M, int64_t N, int64_t ldd) {
-  pdl_wait();
-  pdl_trigger();
-  const float alpha = __ldg(a_ts) * __ldg(b_ts);
-  const int64_t n4 = N / 4, total = M * n4;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t m = i / n4, c = (i - m * n4) * 4;
-    float4 acc = *reinterpret_cast<const float4*>(ws + m * N + c);
-    for (int s = 1; s < splits; ++s) {
-      const float4 v = *reinterpret_cast<const float4*>(ws + ((int64_t)s * M + m) * N + c);
-      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
-    }
-    if constexpr (OUT == MRFP4_DT_BF16) {
-      __nv_bfloat162 lo = __floats2bfloat162_rn(acc.x * alpha, acc.y * alpha);
-      __nv_bfloat162 hi = __floats2bfloat162_rn(acc.z * alpha, acc.w * alpha);
-      *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(d) + m * ldd + c) =
-          make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
-    } else {
-      *reinterpret_cast<float4*>(static_cast<float*>(d) + m * ldd + c) =
-          make_float4(acc.x * alpha, acc.y * alpha, acc.z * alpha, acc.w * alpha);
-    }
-  }
-}
 
 // ---------------------------------------------------------------------------
 // 2-CTA (cta_group::2) kernel: a CTA pair computes a 256 x 256 output tile, persistent
@@ -1087,9 +1119,13 @@ int launch(const uint8_t* a, const uint8_t* b, const GemmArgs& args0, cudaStream
   if (g.ws) {
     int sp = 1, per = g.num_kb;
     splitk_plan(tiles, g.num_kb, &sp, &per);
-    if (sp > 1 && g.ws_bytes >= (size_t)sp * g.M * g.N * sizeof(float)) {
+    if (sp > 1 && g.ws_bytes >= kSplitkHeader + (size_t)sp * g.M * g.N * sizeof(float) &&
+        tiles <= (int)(kSplitkHeader / (2 * sizeof(uint32_t))) && tiles * sp <= num_sms() && g_force_grid == 0 && g.N % 4 == 0 &&
+        g.ldd % 4 == 0) {
       g.splits = sp;
       g.kb_per = per;
+      g.sk_cnt = reinterpret_cast<uint32_t*>(g.ws);
+      g.ws = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(g.ws) + kSplitkHeader);
     }
   }
   const int units = tiles * g.splits;
@@ -1097,13 +1133,6 @@ int launch(const uint8_t* a, const uint8_t* b, const GemmArgs& args0, cudaStream
   if (g_force_grid > 0) grid = std::min(grid, g_force_grid);
   if (launch_pdl(k_gemm_fp4<VEC, BN, OUT>, dim3(grid), dim3(kThreads), C::kSmem, s, tmA, tmB, g) != cudaSuccess)
     return MRFP4_ECUDA;
-  if (g.splits > 1) {
-    const int64_t work = g.M * (g.N / 4);
-    const int rgrid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(work, 256), 4 * num_sms()));
-    if (launch_pdl(k_splitk_reduce<OUT>, dim3(rgrid), dim3(256), 0, s, (const float*)g.ws, g.splits, g.a_ts, g.b_ts,
-                   g.d, g.M, g.N, g.ldd) != cudaSuccess)
-      return MRFP4_ECUDA;
-  }
   return MRFP4_OK;
 }
 
@@ -1156,7 +1185,7 @@ size_t gemm_workspace_bytes(int64_t M, int64_t N, int64_t K) {
   const int tiles = (int)(ceil_div(M, BM) * ceil_div(N, 256));
   int sp = 1, per = 1;
   splitk_plan(tiles, (int)ceil_div(K, BK), &sp, &per);
-  return sp > 1 ? (size_t)sp * M * N * sizeof(float) : 0;
+  return sp > 1 ? kSplitkHeader + (size_t)sp * M * N * sizeof(float) : 0;
 }
 
 int g_debug_mode = 0;

@@ -130,7 +130,7 @@ _WORKSPACE: dict = {}
 
 
 def _gemm_workspace(device: torch.device, stream: int, nbytes: int):
-    """GEMM scratch (split-K partials / stream-K flags + partials), one zero-initialised,
+    """GEMM scratch (split-K tile counters + fp32 partials), one zero-initialised,
     growing buffer per (device, stream) so stream-ordered reuse is safe (every call leaves
     the flag words zero again)."""
     if nbytes == 0:
@@ -138,7 +138,7 @@ def _gemm_workspace(device: torch.device, stream: int, nbytes: int):
     key = (device.index, stream)
     buf = _WORKSPACE.get(key)
     if buf is None or buf.numel() < nbytes:
-        buf = torch.zeros(nbytes, dtype=torch.uint8, device=device)  # stream-K flags start at zero
+        buf = torch.zeros(nbytes, dtype=torch.uint8, device=device)  # split-K counters start at zero
         _WORKSPACE[key] = buf
     return buf
 
