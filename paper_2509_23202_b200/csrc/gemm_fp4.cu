@@ -257,6 +257,38 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     // ------------------------------------------------------------ producer
     if (lane == 0) {
+      auto stage_bytes = [&](int kb, int n_blk) {
+        const int atoms = (int)imin64(C::kAtomsPerKb, g.sf_col_blocks - (int64_t)kb * C::kAtomsPerKb);
+        int nbv = 0;
+#pragma unroll
+        for (int j = 0; j < C::kNB; ++j) nbv += ((int64_t)n_blk * C::kNB + j < g.b_row_blocks);
+        return C::kABytes + C::kBBytes + (uint32_t)atoms * 512u * (1u + nbv);
+      };
+      auto load_weight = [&](int stage, int kb, int n_blk) {
+        const int atoms = (int)imin64(C::kAtomsPerKb, g.sf_col_blocks - (int64_t)kb * C::kAtomsPerKb);
+        const int64_t katom = (int64_t)kb * C::kAtomsPerKb;
+        sm100::tma_load_2d(smem + C::kOffB + stage * C::kBBytes, &tmB, &full[stage], kb * BK_BYTES, n_blk * BN);
+#pragma unroll
+        for (int j = 0; j < C::kNB; ++j) {
+          const int64_t rb = (int64_t)n_blk * C::kNB + j;
+          if (rb < g.b_row_blocks)
+            sm100::bulk_load(smem + C::kOffSfb + stage * C::kSfbBytes + j * C::kAtomsPerKb * 512,
+                             g.b_sf + (rb * g.sf_col_blocks + katom) * 512, atoms * 512u, &full[stage]);
+        }
+      };
+      // The weight half of the first unit's first stages does not depend on the act-quant
+      // kernel: issue it before the PDL wait so the weight stream overlaps K1's tail.
+      int pre = 0;
+      if (blockIdx.x < num_units && g.debug == 0) {
+        const int tile = blockIdx.x / g.splits, split = blockIdx.x - tile * g.splits;
+        const int n_blk = tile / g.num_m_blk;
+        const int kb0 = split * g.kb_per, kb1 = min(g.num_kb, kb0 + g.kb_per);
+        pre = min(kb1 - kb0, C::kStages);
+        for (int i = 0; i < pre; ++i) {
+          sm100::mbar_arrive_expect_tx(&full[i], stage_bytes(kb0 + i, n_blk));   // A + B, all of it
+          load_weight(i, kb0 + i, n_blk);
+        }
+      }
       pdl_wait();  // A, its scale factors and tensor scale come from the act-quant kernel
       int stage = 0;
       uint32_t phase = 0;
@@ -265,30 +297,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int m_blk = tile % g.num_m_blk, n_blk = tile / g.num_m_blk;
         const int kb0 = split * g.kb_per, kb1 = min(g.num_kb, kb0 + g.kb_per);
         for (int kb = kb0; kb < kb1; ++kb) {
-          sm100::mbar_wait(&empty[stage], phase ^ 1);
+          const bool preissued = unit == (int)blockIdx.x && kb - kb0 < pre;
+          if (!preissued) sm100::mbar_wait(&empty[stage], phase ^ 1);
           const int atoms = (int)imin64(C::kAtomsPerKb, g.sf_col_blocks - (int64_t)kb * C::kAtomsPerKb);
-          int nbv = 0;
-#pragma unroll
-          for (int j = 0; j < C::kNB; ++j) nbv += ((int64_t)n_blk * C::kNB + j < g.b_row_blocks);
-          const uint32_t bytes = C::kABytes + C::kBBytes + (uint32_t)atoms * 512u * (1u + nbv);
           if (g.debug == 1 || g.debug == 3 || g.debug == 4 || g.debug == 5) {
             sm100::mbar_arrive(&full[stage]);
             if (++stage == C::kStages) { stage = 0; phase ^= 1; }
             continue;
           }
-          sm100::mbar_arrive_expect_tx(&full[stage], bytes);
+          if (!preissued) {
+            sm100::mbar_arrive_expect_tx(&full[stage], stage_bytes(kb, n_blk));
+            load_weight(stage, kb, n_blk);
+          }
           sm100::tma_load_2d(smem + C::kOffA + stage * C::kABytes, &tmA, &full[stage], kb * BK_BYTES, m_blk * BM);
-          sm100::tma_load_2d(smem + C::kOffB + stage * C::kBBytes, &tmB, &full[stage], kb * BK_BYTES, n_blk * BN);
           const int64_t katom = (int64_t)kb * C::kAtomsPerKb;
           sm100::bulk_load(smem + C::kOffSfa + stage * C::kSfaBytes,
                            g.a_sf + ((int64_t)m_blk * g.sf_col_blocks + katom) * 512, atoms * 512u, &full[stage]);
-#pragma unroll
-          for (int j = 0; j < C::kNB; ++j) {
-            const int64_t rb = (int64_t)n_blk * C::kNB + j;
-            if (rb < g.b_row_blocks)
-              sm100::bulk_load(smem + C::kOffSfb + stage * C::kSfbBytes + j * C::kAtomsPerKb * 512,
-                               g.b_sf + (rb * g.sf_col_blocks + katom) * 512, atoms * 512u, &full[stage]);
-          }
           if (++stage == C::kStages) { stage = 0; phase ^= 1; }
         }
       }
