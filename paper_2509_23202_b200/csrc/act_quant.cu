@@ -605,20 +605,23 @@ __global__ void __launch_bounds__(NW * 32, 768 / (NW * 32))
     for (int i = 0; i < NW; ++i) x = max(x, smax[i]);
     if (x) atomicMax(ws, x);
     if (x >= 0x7f800000u) atomic_or_status(p.status, MRFP4_STATUS_NONFINITE);
-    // ---- grid barrier
-    __threadfence();
-    if (atomicAdd(ws + 1, 1u) == gridDim.x - 1) {
+    // ---- grid barrier without full fences: the arrival is an acq_rel RMW (releases this
+    // CTA's max, acquires every earlier arrival's); the last arriver re-arms the count and
+    // bumps the generation with a release; the others acquire the generation.
+    uint32_t arrived;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(arrived) : "l"(ws + 1) : "memory");
+    if (arrived == gridDim.x - 1) {
       ws[1] = 0u;
-      __threadfence();
-      atomicAdd(ws + 2, 1u);
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ws + 2) : "memory");
     } else {
       uint32_t g;
       do {
         asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(ws + 2) : "memory");
       } while (g == gen0);
     }
-    __threadfence();
-    sk = nv_consts(p, *(volatile uint32_t*)ws);  // fp64 divides: once per CTA, not per warp
+    uint32_t gm;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(gm) : "l"(ws) : "memory");
+    sk = nv_consts(p, gm);  // fp64 divides: once per CTA, not per warp
   }
   __syncthreads();
   tr.mark(4);
@@ -1177,19 +1180,23 @@ __global__ void __launch_bounds__(NW * 32, MB)
     for (int i = 0; i < NW; ++i) x = max(x, smax[i]);
     if (x) atomicMax(ws, x);
     if (x >= 0x7f800000u) atomic_or_status(p.status, MRFP4_STATUS_NONFINITE);
-    __threadfence();
-    if (atomicAdd(ws + 1, 1u) == gridDim.x - 1) {
+    // ---- grid barrier without full fences: the arrival is an acq_rel RMW (releases this
+    // CTA's max, acquires every earlier arrival's); the last arriver re-arms the count and
+    // bumps the generation with a release; the others acquire the generation.
+    uint32_t arrived;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(arrived) : "l"(ws + 1) : "memory");
+    if (arrived == gridDim.x - 1) {
       ws[1] = 0u;
-      __threadfence();
-      atomicAdd(ws + 2, 1u);
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ws + 2) : "memory");
     } else {
       uint32_t g;
       do {
         asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(ws + 2) : "memory");
       } while (g == gen0);
     }
-    __threadfence();
-    sk = nv_consts(p, *(volatile uint32_t*)ws);
+    uint32_t gm;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(gm) : "l"(ws) : "memory");
+    sk = nv_consts(p, gm);
   }
   __syncthreads();
   tr.mark(4);

@@ -14,7 +14,7 @@ for _ in range(3):
     act_quant_into(x, 1, k, a.codes, a.sf, a.tensor_scale_dev, a.scratch)
 buf = torch.zeros(8 * 148 * 24, dtype=torch.int64, device="cuda")
 L.mrfp4_debug_k1_trace(buf.data_ptr())
-flush.zero_(); flush.sum(dtype=torch.int32)
+if not os.environ.get("WARM"): flush.zero_(); flush.sum(dtype=torch.int32)
 act_quant_into(x, 1, k, a.codes, a.sf, a.tensor_scale_dev, a.scratch)
 torch.cuda.synchronize()
 L.mrfp4_debug_k1_trace(None)
@@ -29,3 +29,8 @@ cta = torch.arange(len(t)) // nw
 p1max = t[:, 3].max()
 rel = t[:, 4]
 print("release - global max phase-1 end (us) q0/50/100:", [round(float(torch.quantile((rel - p1max).double(), z)) / 1000, 2) for z in (0, .5, 1)])
+# per CTA: latest phase-1 end, release (us from start)
+for c in range(int(cta.max()) + 1):
+    m = cta == c
+    print("cta", c, "p1 end max", round((t[m, 3].max() - t0).item() / 1000, 2), "release", round((t[m, 4].min() - t0).item() / 1000, 2),
+          "sm", int(t[m, 2][0].item() >> 32), "n", int((t[m, 2] & 0xffffffff).sum().item()))
