@@ -234,6 +234,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // perf traces (null in production): per-CTA globaltimer stamps, 8 slots
+  auto mark = [&](int i) { if (g.dbg) g.dbg[blockIdx.x * 8 + i] = globaltimer(); };
+  if (threadIdx.x == 0) mark(0);
   if (warp == 0 && lane == 0) {
     sm100::tma_prefetch_desc(&tmA);
     sm100::tma_prefetch_desc(&tmB);
@@ -250,6 +253,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  if (threadIdx.x == 0) mark(1);
   pdl_trigger();
 
   const int num_units = g.num_m_blk * g.num_n_blk * g.splits;
@@ -290,6 +294,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       pdl_wait();  // A, its scale factors and tensor scale come from the act-quant kernel
+      mark(2);
       int stage = 0;
       uint32_t phase = 0;
       for (int unit = blockIdx.x; unit < num_units; unit += gridDim.x) {
@@ -331,6 +336,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         sm100::tc_fence_after();
         for (int kb = kb0; kb < kb1; ++kb) {
           sm100::mbar_wait(&full[stage], phase);
+          if (kb == kb0 && unit == (int)blockIdx.x) mark(3);
           sm100::tc_fence_after();
           const uint32_t sfa_t = tmem_base + C::kAccCols + stage * (C::kSfaCols + C::kSfbCols);
           const uint32_t sfb_t = sfa_t + C::kSfaCols;
@@ -371,27 +377,32 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int tile = unit / g.splits, split = unit - tile * g.splits;
       const int m_blk = tile % g.num_m_blk, n_blk = tile / g.num_m_blk;
       sm100::mbar_wait(tfull, acc_phase);
+      if (threadIdx.x == 64 && unit == (int)blockIdx.x) mark(4);
       sm100::tc_fence_after();
       const int64_t row = (int64_t)m_blk * BM + q * 32 + lane;
       // Split-K: lanes past M skip the TMEM read entirely when the whole warp is past M.
       const bool warp_live = (int64_t)m_blk * BM + q * 32 < g.M;
 #pragma unroll 1
-      for (int c = 0; c < ((g.debug >= 3 && g.debug <= 5) || !warp_live ? 0 : BN); c += 32) {
-        uint32_t r[32];
-        sm100::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + c, r);
+      for (int c = 0; c < ((g.debug >= 3 && g.debug <= 5) || !warp_live ? 0 : BN); c += 64) {
+        uint32_t r[2][32];   // two 32-column TMEM loads per wait
+        sm100::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + c, r[0]);
+        sm100::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + c + 32, r[1]);
         sm100::tmem_ld_wait();
-        const int64_t col = (int64_t)n_blk * BN + c;
-        if (row < g.M) {
-          if (g.splits == 1) {
-            store_row32<OUT>(g, row, col, r, alpha);
-          } else {  // fp32 partial, unscaled: ws[split][row][col]
-            float* dst = g.ws + ((int64_t)split * g.M + row) * g.N + col;
 #pragma unroll
-            for (int j = 0; j < 8; ++j)
-              if (col + 4 * j < g.N)
-                *reinterpret_cast<float4*>(dst + 4 * j) =
-                    make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]), __uint_as_float(r[4 * j + 2]),
-                                __uint_as_float(r[4 * j + 3]));
+        for (int h = 0; h < 2; ++h) {
+          const int64_t col = (int64_t)n_blk * BN + c + 32 * h;
+          if (row < g.M) {
+            if (g.splits == 1) {
+              store_row32<OUT>(g, row, col, r[h], alpha);
+            } else {  // fp32 partial, unscaled: ws[split][row][col]
+              float* dst = g.ws + ((int64_t)split * g.M + row) * g.N + col;
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                if (col + 4 * j < g.N)
+                  *reinterpret_cast<float4*>(dst + 4 * j) =
+                      make_float4(__uint_as_float(r[h][4 * j]), __uint_as_float(r[h][4 * j + 1]),
+                                  __uint_as_float(r[h][4 * j + 2]), __uint_as_float(r[h][4 * j + 3]));
+            }
           }
         }
       }
@@ -407,14 +418,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         // [0] partials written, [1] slices reduced; the last slice re-arms both.
         uint32_t* cnt = g.sk_cnt + 2 * tile;
         const int et = threadIdx.x - 64;   // epilogue thread 0..127 (warps 2-5)
-        __threadfence();
         asm volatile("bar.sync 1, 128;" ::: "memory");
         if (et == 0) {
+          mark(5);
+          __threadfence();   // cumulative over the epilogue's stores ordered by the bar.sync
           atomicAdd(cnt, 1u);
           uint32_t seen;
           do {
             asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(cnt) : "memory");
           } while (seen < (uint32_t)g.splits);
+          mark(6);
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");
         __threadfence();
@@ -448,6 +461,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (et == 0) mark(7);
         if (et == 0 && atomicAdd(cnt + 1, 1u) == (uint32_t)g.splits - 1) {
           cnt[0] = 0u;   // every split has passed its wait: re-arm for the next call
           cnt[1] = 0u;
@@ -1192,7 +1206,11 @@ int launch2(const uint8_t* a, const uint8_t* b, const GemmArgs& args0, cudaStrea
 
 void splitk_plan(int tiles, int num_kb, int* splits, int* kb_per) {
   int sp = 1;
-  if (tiles * 2 <= num_sms()) sp = std::min(std::max(1, num_sms() / tiles), std::max(1, num_kb / 2));
+  static const int min_kb = [] {   // k-blocks per split, at least (MRFP4_SK_MINKB: experiments)
+    const char* e = getenv("MRFP4_SK_MINKB");
+    return e ? std::max(1, atoi(e)) : 2;
+  }();
+  if (tiles * 2 <= num_sms()) sp = std::min(std::max(1, num_sms() / tiles), std::max(1, num_kb / min_kb));
   const int per = (int)ceil_div(num_kb, sp);
   *kb_per = per;
   *splits = (int)ceil_div(num_kb, per);
