@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define MRFP4_ABI_VERSION 2
+#define MRFP4_ABI_VERSION 3
 
 /* return codes */
 #define MRFP4_OK 0
@@ -59,6 +59,7 @@ extern "C" {
 #define MRFP4_DT_BF16 0
 #define MRFP4_DT_F16 1
 #define MRFP4_DT_F32 2
+#define MRFP4_DT_F64 3   /* mrfp4_rotate_f64 only (the reference's own float64 inputs) */
 
 /* device status bits */
 #define MRFP4_STATUS_NONFINITE 1u        /* NaN/Inf in the input (quantizers.py:99-100) */
@@ -94,6 +95,43 @@ int mrfp4_act_quant(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ld
                     int fmt, int had_k,
                     uint8_t* codes, uint8_t* sf, float* tensor_scale,
                     uint32_t* status, void* workspace, size_t workspace_bytes, void* stream);
+
+/*
+ * Scale-policy options of mrfp4_act_quant_ex (NULL = the ScalePolicy() defaults of
+ * quantize_rtn, i.e. exactly mrfp4_act_quant):
+ *   mx_four_thirds   MXFP4 only.  1: tensor scale f32(4/3) (quantizers.py:34, :191, :206-207);
+ *                    0: tensor scale 1.0 -- ScalePolicy(e8m0_four_thirds=False).  The E8M0 scale
+ *                    codes are the same; the element codes are rounded against 2^e.
+ *   nv_tensor_scale  NVFP4 only.  NULL: the global scale s_T is derived from the whole tensor's
+ *                    max (quantizers.py:195-200; two-phase launch).  Otherwise a device float s_T
+ *                    used as given (a static / calibrated activation scale):
+ *                    scale codes = E4M3(raw / s_T) saturating at 448, elements saturating at +-6,
+ *                    exactly prepare_scales' arithmetic with that s_global (quantizers.py:157-167,
+ *                    :211-215).  Single pass, no workspace, rows independent.
+ */
+typedef struct mrfp4_act_quant_opts {
+  int mx_four_thirds;
+  const float* nv_tensor_scale;
+} mrfp4_act_quant_opts;
+
+int mrfp4_act_quant_ex(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ldx,
+                       int fmt, int had_k,
+                       uint8_t* codes, uint8_t* sf, float* tensor_scale,
+                       uint32_t* status, void* workspace, size_t workspace_bytes,
+                       const mrfp4_act_quant_opts* opts, void* stream);
+
+/*
+ * apply_blockwise(X, TransformSpec.hadamard(k)) (transforms.py:77-91) for float64 X, as the
+ * reference computes it: y[., j] = sum_i x[., i] * M[i][j] with M = (H_k / sqrt(k))^T, summed
+ * in index order (i = 0 .. k-1, one rounding per term, as an fma chain).  For k = 16 every
+ * product is exact (1/sqrt(16) = 1/4) and this is the order OpenBLAS' dgemm kernel uses for the
+ * reference's X.reshape(rows, K/k, k) @ M at every shape tried (bit-identical in the dev
+ * container); for k in {32, 64, 128} the reference's own result depends on which BLAS kernel
+ * the shape selects (its summation order changes with the shape), so it is not reproducible in
+ * general: this order matches it for some shapes, and is within a few ulp elsewhere.  k = 0: copy.
+ * x: [M, K] float64 row stride ldx; y: [M, K] float64, contiguous.
+ */
+int mrfp4_rotate_f64(const double* x, int64_t M, int64_t K, int64_t ldx, int had_k, double* y, void* stream);
 
 /* QuantResult metrics of an act-quant result (quantizers.py:218-231): accumulates into the
  * caller-zeroed device acc[3] = {sum (y-q)^2, sum y^2, sum over groups of the squared relative

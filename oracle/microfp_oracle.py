@@ -207,7 +207,7 @@ def _format_params(fmt: str):
 
 
 def quantize_rtn(X, fmt: str, hadamard: int | None = None,
-                 four_thirds: bool = True) -> OracleQuant:
+                 four_thirds: bool = True, static_ts: float | None = None) -> OracleQuant:
     """RTN quantization with absmax scales, optionally Hadamard-rotated.
 
     Restates ``quantize_rtn`` (quantizers.py:247-255) for the two hardware
@@ -232,6 +232,8 @@ def quantize_rtn(X, fmt: str, hadamard: int | None = None,
     if fmt == NVFP4:                                               # quantizers.py:198-200
         top = float(amax.max()) / 6.0
         s_glob = float(np.float32(top / E4M3_MAX)) if top > 0 else 1.0
+        if static_ts is not None:   # a given s_global: _encode_raw / _quantize_groups (:157-167, :211-215)
+            s_glob = float(np.float32(static_ts))
         scodes = e4m3_encode(raw / s_glob)                         # quantizers.py:162-167
         dec = E4M3_LEVELS[scodes.astype(np.intp)]
         ts = float(np.float32(s_glob))                             # quantizers.py:191

@@ -17,7 +17,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libmrfp4.so")
 
 OK, EINVAL, EUNSUPPORTED, ECUDA = 0, 1, 2, 3
-DT_BF16, DT_F16, DT_F32 = 0, 1, 2
+DT_BF16, DT_F16, DT_F32, DT_F64 = 0, 1, 2, 3
 STATUS_NONFINITE, STATUS_SCALE_UNDERFLOW = 1, 2
 
 _lock = threading.Lock()
@@ -25,6 +25,11 @@ _lib = None
 
 _c = ctypes
 _vp, _i64, _int, _sz = _c.c_void_p, _c.c_int64, _c.c_int, _c.c_size_t
+
+
+class ActQuantOpts(ctypes.Structure):
+    """mrfp4_act_quant_opts (include/mrfp4.h)."""
+    _fields_ = [("mx_four_thirds", ctypes.c_int), ("nv_tensor_scale", ctypes.c_void_p)]
 SIGNATURES = {
     "mrfp4_abi_version": (_int, []),
     "mrfp4_last_error": (_c.c_char_p, []),
@@ -32,6 +37,9 @@ SIGNATURES = {
     "mrfp4_sf_bytes": (_sz, [_i64, _i64]),
     "mrfp4_act_quant_workspace": (_sz, [_i64, _i64, _int]),
     "mrfp4_act_quant": (_int, [_vp, _int, _i64, _i64, _i64, _int, _int, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "mrfp4_act_quant_ex": (_int, [_vp, _int, _i64, _i64, _i64, _int, _int, _vp, _vp, _vp, _vp, _vp, _sz,
+                                  _c.POINTER(ActQuantOpts), _vp]),
+    "mrfp4_rotate_f64": (_int, [_vp, _i64, _i64, _i64, _int, _vp, _vp]),
     "mrfp4_quant_metrics": (_int, [_vp, _int, _i64, _i64, _i64, _int, _int, _vp, _vp, _vp, _vp, _vp]),
     "mrfp4_sf_swizzle": (_int, [_vp, _vp, _i64, _i64, _vp]),
     "mrfp4_sf_unswizzle": (_int, [_vp, _vp, _i64, _i64, _vp]),
@@ -63,7 +71,7 @@ def lib():
                 for name, (res, args) in SIGNATURES.items():
                     fn = getattr(handle, name)
                     fn.restype, fn.argtypes = res, args
-                if handle.mrfp4_abi_version() != 2:
+                if handle.mrfp4_abi_version() != 3:
                     raise ImportError("libmrfp4.so ABI version mismatch")
                 _lib = handle
     return _lib

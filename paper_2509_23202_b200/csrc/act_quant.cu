@@ -39,6 +39,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <string>
+#include <unordered_map>
 
 #include "common.cuh"
 #include "quant_core.cuh"
@@ -429,15 +431,32 @@ struct EncConsts {
   uint32_t zero_code = 0;
 };
 
-__device__ __forceinline__ EncConsts nv_consts(const AQParams& p, uint32_t gmax_bits) {
+__device__ __forceinline__ EncConsts nv_consts_st(const AQParams& p, float st32) {
   EncConsts k;
-  const double top = (double)__uint_as_float(gmax_bits) * p.c64 / 6.0;  // absmax.max() / FP4_MAX
-  k.st32 = top > 0.0 ? __double2float_rn(top / 448.0) : 1.0f;           // f32(top / E4M3 max)
+  k.st32 = st32;
   k.st64 = (double)k.st32;
   k.zero_code = e4m3_rne64(1.0 / k.st64);                               // raw = 1.0 sentinel
   k.kenc = __double2float_rn(p.c64 / 6.0 / k.st64);
   k.knv = __double2float_rn(p.c64 / k.st64);
   return k;
+}
+
+__device__ __forceinline__ EncConsts nv_consts(const AQParams& p, uint32_t gmax_bits) {
+  const double top = (double)__uint_as_float(gmax_bits) * p.c64 / 6.0;  // absmax.max() / FP4_MAX
+  return nv_consts_st(p, top > 0.0 ? __double2float_rn(top / 448.0) : 1.0f);   // f32(top / E4M3 max)
+}
+
+// Single-pass constants: MXFP4 (tensor scale f32(4/3) or 1.0, quantizers.py:203-207) or NVFP4
+// with a caller-given global scale (read after pdl_wait: a predecessor may produce it).
+template <int FMT>
+__device__ __forceinline__ EncConsts single_pass_consts(const AQParams& p) {
+  if constexpr (FMT == MRFP4_FMT_NVFP4) {
+    return nv_consts_st(p, *p.static_ts);
+  } else {
+    EncConsts k;
+    k.st32 = p.mx_ts;
+    return k;
+  }
 }
 
 // Rotate (already done by the caller) -> scales -> codes -> stores of one lane segment.
@@ -502,20 +521,23 @@ struct Trace {
   }
 };
 
-// MXFP4: single pass (group-local scales).
-template <int IN, int HK, typename W, int NW>
+// Single pass: MXFP4 (group-local scales), or NVFP4 with a caller-given global scale.
+template <int IN, int FMT, int HK, typename W, int NW>
 __global__ void __launch_bounds__(NW * 32, 768 / (NW * 32))
-    k_act_quant_mx(const __grid_constant__ CUtensorMap tmx, AQParams p) {
+    k_act_quant_1p(const __grid_constant__ CUtensorMap tmx, AQParams p) {
   __shared__ uint32_t ctr;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  pdl_trigger();
-  const EncConsts k;
   Trace tr(p, warp, lane);
   if (threadIdx.x == 0) ctr = 0u;
   Loader<IN, W> L;
   init_loader<NW>(L, warp, lane);
   __syncthreads();
   pdl_wait();
+  // Trigger only after the wait: a dependent launched now can only find this grid's
+  // predecessors complete, so its pre-wait loads (the GEMM's weight stream) never race a
+  // kernel two steps back (e.g. K1 of the weight itself).
+  pdl_trigger();
+  const EncConsts k = single_pass_consts<FMT>(p);
   if (blockIdx.x == 0 && threadIdx.x == 0) *p.tensor_scale = k.st32;
   CtaRange r;
   r.init(p);
@@ -528,7 +550,7 @@ __global__ void __launch_bounds__(NW * 32, 768 / (NW * 32))
         u64 P[kPairs];
         load_pairs<IN>(sbase, lane, P);
         if constexpr (HK > 0) fwht<HK>(P, lane, p.pm);
-        encode_seg<MRFP4_FMT_MXFP4>(p, c, P, k, bad);
+        encode_seg<FMT>(p, c, P, k, bad);
       });
   tr.end(n);
   if (bad) atomic_or_status(p.status, bad);
@@ -1062,14 +1084,13 @@ __device__ __forceinline__ void init_mring(MRing<U, S>& R, int warp, int lane) {
 template <int U, int S, int NW>
 constexpr int mring_smem() { return NW * S * (int)MRing<U, S>::kItemBytes + 1024; }
 
-// MXFP4, single pass.  MB: CTAs per SM the register allocation must allow.
-template <int IN, int HK, int U, int S, int NW, int MB>
+// Single pass (MXFP4, or NVFP4 with a given global scale).  MB: CTAs per SM the register
+// allocation must allow.
+template <int IN, int FMT, int HK, int U, int S, int NW, int MB>
 __global__ void __launch_bounds__(NW * 32, MB)
-    k_act_quant_mx_mma(const __grid_constant__ CUtensorMap tmx, AQParams p) {
+    k_act_quant_1p_mma(const __grid_constant__ CUtensorMap tmx, AQParams p) {
   __shared__ uint32_t ctr;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  pdl_trigger();
-  const EncConsts k;
   Trace tr(p, warp, lane);
   if (threadIdx.x == 0) ctr = 0u;
   MRing<U, S> R;
@@ -1089,6 +1110,11 @@ __global__ void __launch_bounds__(NW * 32, MB)
   ldsm_offsets(lane, off);
   __syncthreads();
   pdl_wait();
+  // Trigger only after the wait: a dependent launched now can only find this grid's
+  // predecessors complete, so its pre-wait loads (the GEMM's weight stream) never race a
+  // kernel two steps back (e.g. K1 of the weight itself).
+  pdl_trigger();
+  const EncConsts k = single_pass_consts<FMT>(p);
   if (blockIdx.x == 0 && threadIdx.x == 0) *p.tensor_scale = k.st32;
   CtaRange r;
   r.init(p);
@@ -1102,7 +1128,7 @@ __global__ void __launch_bounds__(NW * 32, MB)
         for (int u = 0; u < U; ++u) {
           u64 P[4][4];
           rotate_tile<IN, HK>(sbase + u * 2048u, off, hbs, lane, P);
-          encode_tile<MRFP4_FMT_MXFP4>(p, k, P, (uint32_t)(item * U + u) * 32u, lane, bad);
+          encode_tile<FMT>(p, k, P, (uint32_t)(item * U + u) * 32u, lane, bad);
         }
       });
   tr.end(n);
@@ -1325,35 +1351,33 @@ __global__ void __launch_bounds__(kMetricWarps * 32) k_quant_metrics(AQParams p,
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
-// Perf-experiment knobs (environment, read per call; unset in production).
+// Perf-experiment knobs (environment, read once per process; unset in production).
 int knob(const char* name, int dflt) {
-  const char* v = std::getenv(name);
-  return v ? std::atoi(v) : dflt;
-}
-
-int num_sms() {
-  static int n = 0;
-  if (n == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
+  static std::mutex mu;
+  static std::unordered_map<std::string, std::pair<bool, int>> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(name);
+  if (it == cache.end()) {
+    const char* v = std::getenv(name);
+    it = cache.emplace(name, std::make_pair(v != nullptr, v ? std::atoi(v) : 0)).first;
   }
-  return n;
+  return it->second.first ? it->second.second : dflt;
 }
 
-// One CTA set per SM that the occupancy calculator allows (cached per kernel).
+int num_sms() { return device_sms(); }
+
+// One CTA set per SM that the occupancy calculator allows (cached per kernel and device).
 template <auto Kern, int NW>
 int launch_persistent(int smem, const CUtensorMap& tm, const AQParams& p, cudaStream_t s) {
-  static std::once_flag once;
-  static int per_sm = -1;
-  std::call_once(once, [&] {
+  static std::atomic<int> cache[kMaxDevices];
+  const int per_sm = per_device_once(cache, [&] {
     int n = 0;
     // Max-shared carveout (the GEMM's too), so K1 -> K2 -> K1 never reconfigures L1/SMEM.
     cudaFuncSetAttribute(Kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
     if (cudaFuncSetAttribute(Kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) == cudaSuccess &&
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, Kern, NW * 32, smem) == cudaSuccess)
-      per_sm = std::max(n, 1);
+      return std::max(n, 1);
+    return -1;
   });
   if (per_sm < 0) return MRFP4_ECUDA;
   const int64_t need = ceil_div(p.items, NW);
@@ -1382,11 +1406,13 @@ template <int IN, int FMT, int HK, int NW>
 int launch_nw(const AQParams& p, const CUtensorMap& tm, cudaStream_t s) {
   constexpr int smem = InCfg<IN>::smem(NW);
   if constexpr (FMT == MRFP4_FMT_NVFP4) {
-    if (p.nseg) return launch_persistent<k_act_quant_nv<IN, HK, FlatWalk, NW>, NW>(smem, tm, p, s);
-    return launch_persistent<k_act_quant_nv<IN, HK, GenWalk, NW>, NW>(smem, tm, p, s);
+    if (!p.static_ts) {
+      if (p.nseg) return launch_persistent<k_act_quant_nv<IN, HK, FlatWalk, NW>, NW>(smem, tm, p, s);
+      return launch_persistent<k_act_quant_nv<IN, HK, GenWalk, NW>, NW>(smem, tm, p, s);
+    }
   }
-  if (p.nseg) return launch_persistent<k_act_quant_mx<IN, HK, FlatWalk, NW>, NW>(smem, tm, p, s);
-  return launch_persistent<k_act_quant_mx<IN, HK, GenWalk, NW>, NW>(smem, tm, p, s);
+  if (p.nseg) return launch_persistent<k_act_quant_1p<IN, FMT, HK, FlatWalk, NW>, NW>(smem, tm, p, s);
+  return launch_persistent<k_act_quant_1p<IN, FMT, HK, GenWalk, NW>, NW>(smem, tm, p, s);
 }
 
 // K1m launch: U tiles per item, S ring stages, NW warps per CTA.
@@ -1397,9 +1423,10 @@ int launch_mma_cfg(AQParams p, cudaStream_t s) {
   if (!make_segment_map<IN>(&tm, p, 32 * U)) return MRFP4_ECUDA;
   p.items = ceil_div((int64_t)p.total_segs, 32 * U);
   constexpr int smem = mring_smem<U, S, NW>();
-  if constexpr (FMT == MRFP4_FMT_NVFP4)
-    return launch_persistent<k_act_quant_nv_mma<IN, HK, U, S, NW, MB>, NW>(smem, tm, p, s);
-  return launch_persistent<k_act_quant_mx_mma<IN, HK, U, S, NW, MB>, NW>(smem, tm, p, s);
+  if constexpr (FMT == MRFP4_FMT_NVFP4) {
+    if (!p.static_ts) return launch_persistent<k_act_quant_nv_mma<IN, HK, U, S, NW, MB>, NW>(smem, tm, p, s);
+  }
+  return launch_persistent<k_act_quant_1p_mma<IN, FMT, HK, U, S, NW, MB>, NW>(smem, tm, p, s);
 }
 
 // Two tiles per item (fewer claims / TMA issues per tile) once every warp gets >= 8 tiles;
@@ -1506,15 +1533,24 @@ AQParams make_params(const void* x, int64_t M, int64_t K, int64_t ldx, int fmt, 
   }
   p.c64 = hk ? 1.0 / sqrt((double)hk) : 1.0;
   p.kraw = (float)(p.c64 / 6.0);
-  p.kmx = (float)(p.c64 / (double)1.33333337306976318359375f);
+  p.mx_ts = 1.33333337306976318359375f;   // f32(4/3), quantizers.py:34, :191
+  p.kmx = (float)(p.c64 / (double)p.mx_ts);
+  p.static_ts = nullptr;
   return p;
 }
 }  // namespace
 
 int launch_act_quant(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ldx, int fmt, int hk,
                      uint8_t* codes, uint8_t* sf, float* tensor_scale, uint32_t* status,
-                     void* workspace, cudaStream_t s) {
+                     void* workspace, const mrfp4_act_quant_opts* opts, cudaStream_t s) {
   AQParams p = make_params(x, M, K, ldx, fmt, hk, codes, sf, tensor_scale, status, workspace, true);
+  if (opts) {
+    if (fmt == MRFP4_FMT_MXFP4 && !opts->mx_four_thirds) {
+      p.mx_ts = 1.0f;   // ScalePolicy(e8m0_four_thirds=False): quantizers.py:206-207
+      p.kmx = (float)p.c64;
+    }
+    if (fmt == MRFP4_FMT_NVFP4) p.static_ts = opts->nv_tensor_scale;
+  }
   p.x_bytes = (uint64_t)M * (uint64_t)K * (x_dtype == MRFP4_DT_F32 ? 4u : 2u);
   p.marks = knob("MRFP4_K1_MARKS", -1);
   int rc;

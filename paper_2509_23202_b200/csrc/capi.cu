@@ -11,7 +11,9 @@
 
 namespace mrfp4 {
 int launch_act_quant(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ldx, int fmt, int hk, uint8_t* codes,
-                     uint8_t* sf, float* tensor_scale, uint32_t* status, void* workspace, cudaStream_t s);
+                     uint8_t* sf, float* tensor_scale, uint32_t* status, void* workspace,
+                     const mrfp4_act_quant_opts* opts, cudaStream_t s);
+int launch_rotate_f64(const double* x, int64_t M, int64_t K, int64_t ldx, int hk, double* y, cudaStream_t s);
 int launch_gemm_fp4(const uint8_t* a, const uint8_t* a_sf, const float* a_ts, const uint8_t* b, const uint8_t* b_sf,
                     const float* b_ts, void* d, int d_dtype, int64_t M, int64_t N, int64_t K, int64_t ldd, int fmt,
                     void* ws, size_t ws_bytes, cudaStream_t s);
@@ -95,6 +97,13 @@ size_t mrfp4_act_quant_workspace(int64_t, int64_t, int fmt) { return fmt == MRFP
 int mrfp4_act_quant(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ldx, int fmt, int had_k, uint8_t* codes,
                     uint8_t* sf, float* tensor_scale, uint32_t* status, void* workspace, size_t workspace_bytes,
                     void* stream) {
+  return mrfp4_act_quant_ex(x, x_dtype, M, K, ldx, fmt, had_k, codes, sf, tensor_scale, status, workspace,
+                            workspace_bytes, nullptr, stream);
+}
+
+int mrfp4_act_quant_ex(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ldx, int fmt, int had_k,
+                       uint8_t* codes, uint8_t* sf, float* tensor_scale, uint32_t* status, void* workspace,
+                       size_t workspace_bytes, const mrfp4_act_quant_opts* opts, void* stream) {
   const int G = mrfp4_group_size(fmt);
   if (G == 0) return fail(MRFP4_EUNSUPPORTED, "unknown format %d", fmt);
   const int es = elt_size(x_dtype);
@@ -112,11 +121,25 @@ int mrfp4_act_quant(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ld
   if (((uint64_t)ldx * es) % 16 || !aligned(x, 16))
     return fail(MRFP4_EUNSUPPORTED, "input rows must be 16-byte aligned");
   if (!aligned(codes, 16) || !aligned(sf, 2)) return fail(MRFP4_EUNSUPPORTED, "output buffers must be 16-byte aligned");
-  if (fmt == MRFP4_FMT_NVFP4 && (workspace == nullptr || workspace_bytes < 16 || !aligned(workspace, 4)))
+  const bool nv_static = fmt == MRFP4_FMT_NVFP4 && opts && opts->nv_tensor_scale;
+  if (nv_static && !aligned(opts->nv_tensor_scale, 4)) return fail(MRFP4_EINVAL, "misaligned nv_tensor_scale");
+  if (fmt == MRFP4_FMT_NVFP4 && !nv_static &&
+      (workspace == nullptr || workspace_bytes < 16 || !aligned(workspace, 4)))
     return fail(MRFP4_EINVAL, "NVFP4 needs a 16-byte, 4-byte aligned, zero-initialised device workspace");
   const int rc = mrfp4::launch_act_quant(x, x_dtype, M, K, ldx, fmt, had_k, codes, sf, tensor_scale, status,
-                                         workspace, static_cast<cudaStream_t>(stream));
+                                         workspace, opts, static_cast<cudaStream_t>(stream));
   return cuda_status(rc, "mrfp4_act_quant");
+}
+
+int mrfp4_rotate_f64(const double* x, int64_t M, int64_t K, int64_t ldx, int had_k, double* y, void* stream) {
+  if (M < 1 || K < 1) return fail(MRFP4_EINVAL, "expected a non-empty 2-D matrix");
+  if (had_k != 0 && had_k != 16 && had_k != 32 && had_k != 64 && had_k != 128)
+    return fail(MRFP4_EUNSUPPORTED, "unsupported Hadamard block %d (GPU path: 16, 32, 64, 128)", had_k);
+  if (had_k && K % had_k)
+    return fail(MRFP4_EINVAL, "columns (%lld) not divisible by transform block (%d)", (long long)K, had_k);
+  if (ldx < K || !x || !y) return fail(MRFP4_EINVAL, "bad arguments");
+  return cuda_status(mrfp4::launch_rotate_f64(x, M, K, ldx, had_k, y, static_cast<cudaStream_t>(stream)),
+                     "mrfp4_rotate_f64");
 }
 
 int mrfp4_quant_metrics(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ldx, int fmt, int had_k,

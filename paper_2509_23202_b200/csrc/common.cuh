@@ -1,5 +1,6 @@
 // Shared helpers for the mrfp4 sm_100a kernels (B200).
 #pragma once
+#include <atomic>
 #include <cstdint>
 #include <utility>
 #include <cuda_runtime.h>
@@ -50,6 +51,41 @@ __device__ __forceinline__ void atomic_or_status(uint32_t* status, uint32_t bits
 // pdl_trigger() lets the successor's CTAs launch (they still wait in pdl_wait()).
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// ---------------------------------------------------------------------------
+// Per-device host state.  Kernel attributes (max dynamic SMEM, carveout) and occupancy are
+// per device, so every cache is an array indexed by the calling thread's current device.
+// Entries are atomics: concurrent first calls may both compute the (idempotent) value.
+// ---------------------------------------------------------------------------
+constexpr int kMaxDevices = 64;
+inline int current_device() {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= kMaxDevices) d = 0;
+  return d;
+}
+inline int device_sms() {
+  static std::atomic<int> n[kMaxDevices];
+  const int d = current_device();
+  int v = n[d].load(std::memory_order_relaxed);
+  if (v <= 0) {
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d) != cudaSuccess || v <= 0) v = 148;
+    n[d].store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
+// Runs `init()` (returning > 0 on success, <= 0 on failure) once per device for the cache
+// `slot` (one static array per kernel instantiation) and returns its cached result.
+template <typename F>
+inline int per_device_once(std::atomic<int> (&slot)[kMaxDevices], F&& init) {
+  const int d = current_device();
+  int v = slot[d].load(std::memory_order_acquire);
+  if (v == 0) {
+    v = init();
+    if (v == 0) v = -1;
+    slot[d].store(v, std::memory_order_release);
+  }
+  return v;
+}
 
 // Launch `kern` on `s` with the PDL attribute (disabled when MRFP4_PDL=0 in the environment).
 bool pdl_enabled();

@@ -1120,27 +1120,17 @@ bool make_code_map3(CUtensorMap* tm, const uint8_t* ptr, int64_t rows, int64_t K
 // least 2 k-blocks per split.
 void splitk_plan(int tiles, int num_kb, int* splits, int* kb_per);
 
-int num_sms() {
-  static int n = 0;
-  if (n == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
-}
+int num_sms() { return device_sms(); }
 
 template <int VEC, int BN, int OUT>
 int launch(const uint8_t* a, const uint8_t* b, const GemmArgs& args0, cudaStream_t s) {
   using C = Cfg<VEC, BN>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    if (cudaFuncSetAttribute(k_gemm_fp4<VEC, BN, OUT>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem) !=
-        cudaSuccess)
-      return MRFP4_ECUDA;
-    attr_set = true;
-  }
+  static std::atomic<int> attr[kMaxDevices];   // per device: the attribute is per context
+  if (per_device_once(attr, [] {
+        return cudaFuncSetAttribute(k_gemm_fp4<VEC, BN, OUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    C::kSmem) == cudaSuccess ? 1 : -1;
+      }) < 0)
+    return MRFP4_ECUDA;
   GemmArgs g = args0;
   CUtensorMap tmA, tmB;
   if (!make_code_map(&tmA, a, g.M, g.K, BM) || !make_code_map(&tmB, b, g.N, g.K, BN)) return MRFP4_ECUDA;
@@ -1177,13 +1167,12 @@ int launch(const uint8_t* a, const uint8_t* b, const GemmArgs& args0, cudaStream
 template <int VEC, int OUT, int HKQ = 0>
 int launch2(const uint8_t* a, const uint8_t* b, const GemmArgs& args0, cudaStream_t s) {
   using C = Cfg2<VEC>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    if (cudaFuncSetAttribute(k_gemm_fp4_2sm<VEC, OUT, HKQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem) !=
-        cudaSuccess)
-      return MRFP4_ECUDA;
-    attr_set = true;
-  }
+  static std::atomic<int> attr[kMaxDevices];
+  if (per_device_once(attr, [] {
+        return cudaFuncSetAttribute(k_gemm_fp4_2sm<VEC, OUT, HKQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    C::kSmem) == cudaSuccess ? 1 : -1;
+      }) < 0)
+    return MRFP4_ECUDA;
   GemmArgs g = args0;
   CUtensorMap tmA, tmB;
   const int64_t sfc = g.K / VEC;

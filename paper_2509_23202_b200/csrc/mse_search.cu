@@ -189,6 +189,27 @@ int grid_for(int64_t n) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 128), (int64_t)sms * 16));
 }
 
+// apply_blockwise for float64 X (transforms.py:77-91): y[r, b + j] = sum_i x[r, b + i] * M[i][j],
+// M = (H_k / sqrt(k))^T with entries +-RN64(1 / RN64(sqrt(k))), summed in index order as an fma
+// chain (see mrfp4.h: the reference's BLAS order for k = 16, where every product is exact).
+__global__ void __launch_bounds__(256) k_rotate_f64(const double* __restrict__ x, int64_t M, int64_t K, int64_t ldx,
+                                                    int hk, double c, double* __restrict__ y) {
+  const int64_t total = M * K;
+  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < total; o += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = o / K, col = o - r * K;
+    const double* xr = x + r * ldx;
+    if (hk == 0) {
+      y[o] = xr[col];
+      continue;
+    }
+    const int j = (int)(col % hk);
+    const int64_t b = col - j;
+    double acc = xr[b] * c;                       // i = 0: H[0][j] = +1
+    for (int i = 1; i < hk; ++i) acc = fma(xr[b + i], (__popc(i & j) & 1) ? -c : c, acc);
+    y[o] = acc;
+  }
+}
+
 }  // namespace
 
 int launch_mse_pass(const double* y, int64_t ngroups, int fmt, const double* cand, int ncand, const double* raw0,
@@ -211,6 +232,12 @@ int launch_mse_group_err(const double* y, int64_t ngroups, int fmt, const double
     k_mse_group_err<32><<<grid, 128, 0, s>>>(y, ngroups, dec, ts, gerr, status);
   else
     k_mse_group_err<16><<<grid, 128, 0, s>>>(y, ngroups, dec, ts, gerr, status);
+  return cudaPeekAtLastError() == cudaSuccess ? MRFP4_OK : MRFP4_ECUDA;
+}
+
+int launch_rotate_f64(const double* x, int64_t M, int64_t K, int64_t ldx, int hk, double* y, cudaStream_t s) {
+  const double c = hk ? 1.0 / std::sqrt((double)hk) : 1.0;   // _sylvester(k) / np.sqrt(k)
+  k_rotate_f64<<<grid_for(M * K), 256, 0, s>>>(x, M, K, ldx, hk, c, y);
   return cudaPeekAtLastError() == cudaSuccess ? MRFP4_OK : MRFP4_ECUDA;
 }
 

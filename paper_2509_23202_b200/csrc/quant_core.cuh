@@ -33,7 +33,9 @@ struct AQParams {
   int lane_bits;           // log2(L)
   double c64;              // RN64(1 / RN64(sqrt(k)))  (transforms.py:65: H / np.sqrt(k))
   float kraw;              // MXFP4: ~ c / 6
-  float kmx;               // MXFP4: ~ c / f32(4/3)
+  float kmx;               // MXFP4: ~ c / ts
+  float mx_ts;             // MXFP4 tensor scale: f32(4/3), or 1.0 for e8m0_four_thirds=False
+  const float* static_ts;  // NVFP4: device s_T given by the caller (single pass), or null
   unsigned long long pm;   // f32x2 (1, -1): FWHT h = 1 signs, a uniform-register operand of FFMA2
   int Mi, Ki;              // M, K as 32-bit (the C-ABI checks they fit)
   uint32_t half_k;         // K / 2: bytes per code row

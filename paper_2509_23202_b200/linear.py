@@ -28,7 +28,7 @@ import torch
 from . import _lib
 from .errors import DataError
 from .formats import FMT_MXFP4 as FMT_MXFP4_CODE, FMT_NVFP4 as FMT_NVFP4_CODE, GROUP, format_code, spec_for
-from .quantize import GpuQuantResult, act_quant_into, alloc_result, as_device_matrix, quantize_rtn
+from .quantize import GpuQuantResult, act_quant_into, alloc_result, as_device_matrix, quantize_rtn, stream_scratch
 from .transforms import hadamard_block, transform_for
 
 _OUT = {torch.bfloat16: _lib.DT_BF16, torch.float32: _lib.DT_F32}
@@ -82,7 +82,12 @@ def prepare_weight(w, device=None) -> PackedWeight:
         return w
     if isinstance(w, GpuQuantResult):
         _validate_gemm_k(w.cols)
-        return PackedWeight(w.fmt, w.had_k, w.rows, w.cols, w.codes, w.sf, w.tensor_scale_dev)
+        # The clone is a plain stream-ordered copy, i.e. an ordering point outside the PDL chain:
+        # the GEMM issues its weight loads before griddepcontrol.wait, so it must never become a
+        # programmatic dependent of the K1 launch still writing this weight.
+        with torch.cuda.device(w.codes.device):
+            ts = w.tensor_scale_dev.clone()
+        return PackedWeight(w.fmt, w.had_k, w.rows, w.cols, w.codes, w.sf, ts)
     if isinstance(w, (str, os.PathLike)):
         from .fileio import read_quant
         w, _perm = read_quant(w)  # the permutation section is informational (codes are un-permuted)
@@ -130,9 +135,10 @@ _WORKSPACE: dict = {}
 
 
 def _gemm_workspace(device: torch.device, stream: int, nbytes: int):
-    """GEMM scratch (split-K tile counters + fp32 partials), one zero-initialised,
-    growing buffer per (device, stream) so stream-ordered reuse is safe (every call leaves
-    the flag words zero again)."""
+    """GEMM scratch (split-K tile counters + fp32 partials) for eager calls: one zero-initialised,
+    growing buffer per (device, stream), so stream-ordered reuse is safe (every call leaves
+    the counter words zero again).  CUDA graphs must not use it (a later, larger request
+    replaces -- frees -- the buffer a graph captured): ``GraphedLinear`` owns its workspace."""
     if nbytes == 0:
         return None
     key = (device.index, stream)
@@ -143,20 +149,48 @@ def _gemm_workspace(device: torch.device, stream: int, nbytes: int):
     return buf
 
 
-def gemm(a: GpuQuantResult, w: PackedWeight, out: torch.Tensor) -> torch.Tensor:
-    """K2 only: out[M, N] = a . w^T with both operands already quantized."""
+def gemm_workspace_bytes(M: int, w: PackedWeight) -> int:
+    return int(_lib.lib().mrfp4_gemm_workspace(M, w.N, w.K, w.fmt))
+
+
+def _check_out(out: torch.Tensor, M: int, w: PackedWeight) -> None:
+    if not isinstance(out, torch.Tensor) or out.dtype not in _OUT:
+        raise DataError("out must be a torch.bfloat16 or torch.float32 tensor")
+    if out.device != w.device:
+        raise DataError(f"out is on {out.device}, the weight on {w.device}")
+    if out.dim() != 2 or tuple(out.shape) != (M, w.N):
+        raise DataError(f"out must have shape ({M}, {w.N}), got {tuple(out.shape)}")
+    if out.stride(1) != 1 or out.stride(0) < w.N:
+        raise DataError("out must be row-major with unit column stride")
+
+
+def gemm(a: GpuQuantResult, w: PackedWeight, out: torch.Tensor, ws: torch.Tensor | None = None) -> torch.Tensor:
+    """K2 only: out[M, N] = a . w^T with both operands already quantized.  ``ws``: an explicit,
+    zero-initialised split-K workspace of ``gemm_workspace_bytes`` bytes (CUDA graphs);
+    default: the per-(device, stream) eager workspace."""
     if a.fmt != w.fmt or a.cols != w.K:
         raise DataError("activation / weight format or K mismatch")
+    if a.codes.device != w.device:
+        raise DataError(f"activation on {a.codes.device}, weight on {w.device}")
+    _check_out(out, a.rows, w)
     L = _lib.lib()
-    stream = _lib.stream_ptr(torch, out.device)
-    nbytes = L.mrfp4_gemm_workspace(a.rows, w.N, w.K, w.fmt)
-    ws = _gemm_workspace(out.device, stream, nbytes)
+    with torch.cuda.device(out.device):
+        stream = _lib.stream_ptr(torch, out.device)
+        nbytes = L.mrfp4_gemm_workspace(a.rows, w.N, w.K, w.fmt)
+        if ws is None:
+            ws = _gemm_workspace(out.device, stream, nbytes)
+        elif ws.numel() < nbytes or ws.device != out.device:
+            raise DataError(f"workspace needs {nbytes} bytes on {out.device}")
+        _gemm_launch(L, a, w, out, ws, nbytes, stream)
+    return out
+
+
+def _gemm_launch(L, a, w, out, ws, nbytes, stream):
     _lib.check(L.mrfp4_gemm(
         _lib.ptr(a.codes), _lib.ptr(a.sf), _lib.ptr(a.tensor_scale_dev),
         _lib.ptr(w.codes), _lib.ptr(w.sf), _lib.ptr(w.tensor_scale_dev),
         _lib.ptr(out), _OUT[out.dtype], a.rows, w.N, w.K, out.stride(0), w.fmt,
         _lib.ptr(ws), nbytes, stream))
-    return out
 
 
 def quantized_linear(x, w: PackedWeight, *, out_dtype=torch.bfloat16, out: torch.Tensor | None = None,
@@ -171,7 +205,8 @@ def quantized_linear(x, w: PackedWeight, *, out_dtype=torch.bfloat16, out: torch
     M, K = x2.shape
     if K != w.K:
         raise DataError(f"activation K={K} does not match weight K={w.K}")
-    a = alloc_result(M, K, w.fmt, w.had_k, x2.device)
+    # check=False never reads the status word: reuse the stream's scratch (no zero-fill launch)
+    a = alloc_result(M, K, w.fmt, w.had_k, x2.device, None if check else stream_scratch(x2.device))
     act_quant_into(x2, w.fmt, w.had_k, a.codes, a.sf, a.tensor_scale_dev, a.scratch)
     if check:
         a.check()
@@ -324,6 +359,10 @@ class GraphedLinear:
         self.x = torch.zeros((M, w.K), dtype=x_dtype, device=dev)
         self.y = torch.empty((M, w.N), dtype=out_dtype, device=dev)
         self.a = alloc_result(M, w.K, w.fmt, w.had_k, dev)
+        # The graph captures raw pointers: it owns its split-K workspace (zeroed once; every
+        # replay leaves the counters zero again) instead of borrowing the shared eager one.
+        nbytes = gemm_workspace_bytes(M, w)
+        self.ws = torch.zeros(max(nbytes, 1), dtype=torch.uint8, device=dev)
         side = torch.cuda.Stream(dev)
         side.wait_stream(torch.cuda.current_stream(dev))
         with torch.cuda.stream(side):
@@ -339,7 +378,7 @@ class GraphedLinear:
     def _run(self):
         act_quant_into(self.x, self.w.fmt, self.w.had_k, self.a.codes, self.a.sf, self.a.tensor_scale_dev,
                        self.a.scratch)
-        gemm(self.a, self.w, self.y)
+        gemm(self.a, self.w, self.y, ws=self.ws)
 
     def __call__(self, x: torch.Tensor | None = None) -> torch.Tensor:
         """Replay on the current stream; ``x`` (same shape) is copied into the static input first.

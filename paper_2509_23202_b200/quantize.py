@@ -8,8 +8,11 @@ device buffers in the layout the GEMM consumes (codes [M, K/2], swizzled scale
 factors, device tensor scale) and converts to the reference container on demand
 (``.tensor`` / ``.to_mfp()``).
 
-Numerics: bf16 / fp16 / fp32 inputs are exact in the kernel's fp32 registers; a
-float64 input is rounded to fp32 first (the reference works in float64).
+Numerics: bf16 / fp16 / fp32 inputs are exact in the kernel's fp32 registers.  A float64
+input (the reference's own dtype, quantizers.py:96) takes a float64 device path instead:
+``mrfp4_rotate_f64`` (the reference's summation order) and the float64 encoder of
+``mrfp4_mse_pass`` with the single candidate 1.0 -- prepare_scales + _assemble
+(quantizers.py:170-215) in the reference's arithmetic.
 """
 
 from __future__ import annotations
@@ -38,8 +41,10 @@ def _check_policy(policy, fmt: int, mse: bool = False) -> None:
         return
     if getattr(policy, "scale_fit", None) is not None:
         raise DataError("unsupported on GPU path: scale_fit (fitted E8M0 grid is not hardware E8M0)")
-    if fmt != FMT_NVFP4 and not getattr(policy, "e8m0_four_thirds", True) and not mse:
-        raise DataError("unsupported on GPU path: e8m0_four_thirds=False")
+
+
+def _mx_four_thirds(policy) -> bool:
+    return True if policy is None else bool(getattr(policy, "e8m0_four_thirds", True))
 
 
 def as_device_matrix(X, device=None) -> torch.Tensor:
@@ -50,10 +55,8 @@ def as_device_matrix(X, device=None) -> torch.Tensor:
         X = torch.from_numpy(np.ascontiguousarray(np.asarray(X)))
     if X.dim() != 2 or X.shape[0] < 1 or X.shape[1] < 1:
         raise DataError("expected a non-empty 2-D matrix")
-    if X.dtype == torch.float64:
-        X = X.to(torch.float32)
-    elif X.dtype not in _DT:
-        X = X.to(torch.float32)
+    if X.dtype not in _DT and X.dtype != torch.float64:
+        X = X.to(torch.float64 if X.dtype in (torch.int64, torch.int32) else torch.float32)
     if X.device.type != "cuda":
         X = X.to(device or "cuda", non_blocking=False)
     es = X.element_size()
@@ -110,8 +113,9 @@ class GpuQuantResult:
     def scale_codes(self) -> torch.Tensor:
         """Row-major [rows, cols // G] scale codes on the device (unswizzled)."""
         out = torch.empty((self.rows, self.cols // self.group_size), dtype=torch.uint8, device=self.codes.device)
-        _lib.check(_lib.lib().mrfp4_sf_unswizzle(_lib.ptr(self.sf), _lib.ptr(out), self.rows, out.shape[1],
-                                                 _lib.stream_ptr(torch, self.codes.device)))
+        with torch.cuda.device(self.codes.device):
+            _lib.check(_lib.lib().mrfp4_sf_unswizzle(_lib.ptr(self.sf), _lib.ptr(out), self.rows, out.shape[1],
+                                                     _lib.stream_ptr(torch, self.codes.device)))
         return out
 
     def to_mfp(self) -> MfpTensor:
@@ -132,10 +136,11 @@ class GpuQuantResult:
                 raise DataError("metrics need the quantized input (result built without a source)")
             X = self.source
             acc = torch.zeros(3, dtype=torch.float64, device=self.codes.device)
-            _lib.check(_lib.lib().mrfp4_quant_metrics(
-                _lib.ptr(X), _DT[X.dtype], self.rows, self.cols, X.stride(0), self.fmt, self.had_k,
-                _lib.ptr(self.codes), _lib.ptr(self.sf), _lib.ptr(self.tensor_scale_dev), _lib.ptr(acc),
-                _lib.stream_ptr(torch, X.device)))
+            with torch.cuda.device(X.device):
+                _lib.check(_lib.lib().mrfp4_quant_metrics(
+                    _lib.ptr(X), _DT[X.dtype], self.rows, self.cols, X.stride(0), self.fmt, self.had_k,
+                    _lib.ptr(self.codes), _lib.ptr(self.sf), _lib.ptr(self.tensor_scale_dev), _lib.ptr(acc),
+                    _lib.stream_ptr(torch, X.device)))
             e2, x2, top = acc.tolist()
             n_groups = self.rows * (self.cols // self.group_size)
             self._metrics = (e2 / x2 if x2 > 0 else 0.0, top / n_groups)
@@ -151,16 +156,42 @@ class GpuQuantResult:
 
 
 def act_quant_into(X: torch.Tensor, fmt: int, had_k: int, codes: torch.Tensor, sf: torch.Tensor,
-                   ts: torch.Tensor, scratch: torch.Tensor) -> None:
-    """Launch K1 on the current stream into caller-provided buffers (no allocation)."""
+                   ts: torch.Tensor, scratch: torch.Tensor, *, four_thirds: bool = True,
+                   static_ts: torch.Tensor | None = None) -> None:
+    """Launch K1 on the current stream into caller-provided buffers (no allocation).
+    ``four_thirds=False``: MXFP4 tensor scale 1.0 (ScalePolicy(e8m0_four_thirds=False));
+    ``static_ts``: NVFP4 with a given device global scale (single pass)."""
     M, K = X.shape
     L = _lib.lib()
-    _lib.check(L.mrfp4_act_quant(_lib.ptr(X), _DT[X.dtype], M, K, X.stride(0), fmt, had_k,
-                                 _lib.ptr(codes), _lib.ptr(sf), _lib.ptr(ts), _lib.ptr(scratch),
-                                 _lib.ptr(scratch) + 16, 32, _lib.stream_ptr(torch, X.device)))
+    opts = None
+    if not four_thirds or static_ts is not None:
+        if static_ts is not None and (static_ts.dtype != torch.float32 or static_ts.device != X.device):
+            raise DataError("static tensor scale must be a float32 tensor on the input's device")
+        opts = _lib.ActQuantOpts(int(four_thirds), _lib.ptr(static_ts) if static_ts is not None else None)
+    with torch.cuda.device(X.device):   # launch on the tensors' device, not the current one
+        _lib.check(L.mrfp4_act_quant_ex(_lib.ptr(X), _DT[X.dtype], M, K, X.stride(0), fmt, had_k,
+                                        _lib.ptr(codes), _lib.ptr(sf), _lib.ptr(ts), _lib.ptr(scratch),
+                                        _lib.ptr(scratch) + 16, 32,
+                                        _lib.ctypes.byref(opts) if opts is not None else None,
+                                        _lib.stream_ptr(torch, X.device)))
 
 
-def alloc_result(M: int, K: int, fmt: int, had_k: int, device) -> GpuQuantResult:
+_SCRATCH: dict = {}
+
+
+def stream_scratch(device) -> torch.Tensor:
+    """K1 scratch shared by the stream-ordered calls that never read the status word
+    (``quantized_linear(check=False)``): zeroed once; the NVFP4 workspace words re-arm
+    themselves at the end of every launch, so no per-call zero-fill kernel is needed."""
+    device = torch.device(device)
+    key = (device.index, torch.cuda.current_stream(device).cuda_stream)
+    buf = _SCRATCH.get(key)
+    if buf is None:
+        buf = _SCRATCH[key] = torch.zeros(12, dtype=torch.int32, device=device)
+    return buf
+
+
+def alloc_result(M: int, K: int, fmt: int, had_k: int, device, scratch: torch.Tensor | None = None) -> GpuQuantResult:
     G = GROUP[fmt]
     sfb = _lib.lib().mrfp4_sf_bytes(M, K // G)
     return GpuQuantResult(
@@ -168,20 +199,26 @@ def alloc_result(M: int, K: int, fmt: int, had_k: int, device) -> GpuQuantResult
         torch.empty((M, K // 2), dtype=torch.uint8, device=device),
         torch.empty(sfb, dtype=torch.uint8, device=device),
         torch.empty(1, dtype=torch.float32, device=device),
-        torch.zeros(12, dtype=torch.int32, device=device))
+        scratch if scratch is not None else torch.zeros(12, dtype=torch.int32, device=device))
 
 
-def quantize_rtn(X, spec, policy=None, transform=None, *, check: bool = True) -> GpuQuantResult:
+def quantize_rtn(X, spec, policy=None, transform=None, *, check: bool = True,
+                 static_tensor_scale=None) -> GpuQuantResult:
     """Round-to-nearest FP4 quantization with absmax scales, on the GPU.
 
     Drop-in for ``microfp.quantize_rtn`` (quantizers.py:247-255) for the MXFP4 /
-    NVFP4 presets and Hadamard blocks 16/32/64/128 (or no transform).
+    NVFP4 presets and Hadamard blocks 16/32/64/128 (or no transform), including
+    ``ScalePolicy(e8m0_four_thirds=False)`` (quantizers.py:206-207) and float64 input.
     ``check=True`` (the reference behaviour) synchronizes to raise ``DataError`` on
     non-finite data; pass ``check=False`` to stay asynchronous and call
     ``.check()`` later.
+    ``static_tensor_scale`` (NVFP4, not in the reference API): a precomputed global scale s_T
+    (float or device float32 tensor) replacing the whole-tensor max --
+    one pass, rows independent; codes are prepare_scales' with that s_global.
     """
     fmt = format_code(spec)
     _check_policy(policy, fmt)
+    four_thirds = _mx_four_thirds(policy)
     had_k = hadamard_block(transform)
     X = as_device_matrix(X)
     M, K = X.shape
@@ -190,9 +227,86 @@ def quantize_rtn(X, spec, policy=None, transform=None, *, check: bool = True) ->
         raise DataError(f"columns ({K}) not divisible by group size ({G})")
     if had_k and K % had_k:                                         # quantizers.py:108-111
         raise DataError(f"columns ({K}) not divisible by transform block ({had_k})")
+    st = _static_ts(static_tensor_scale, fmt, X.device)
+    if X.dtype == torch.float64:
+        return _quantize_rtn_f64(X, fmt, had_k, four_thirds, st, check)
     res = alloc_result(M, K, fmt, had_k, X.device)
-    act_quant_into(X, fmt, had_k, res.codes, res.sf, res.tensor_scale_dev, res.scratch)
+    act_quant_into(X, fmt, had_k, res.codes, res.sf, res.tensor_scale_dev, res.scratch,
+                   four_thirds=four_thirds, static_ts=st)
     res.source = X
+    if check:
+        res.check()
+    return res
+
+
+def _static_ts(value, fmt: int, device) -> torch.Tensor | None:
+    if value is None:
+        return None
+    if fmt != FMT_NVFP4:
+        raise DataError("static_tensor_scale applies to NVFP4 only (MXFP4 has no global scale)")
+    t = value if isinstance(value, torch.Tensor) else torch.tensor([float(value)], dtype=torch.float32)
+    t = t.to(device=device, dtype=torch.float32).reshape(1)
+    if not isinstance(value, torch.Tensor) and not (np.isfinite(float(value)) and float(value) > 0):
+        raise DataError("static tensor scale must be finite and positive")
+    return t
+
+
+_FP4_MAG = (0.0, 0.5, 1.0, 1.5, 2.0, 3.0, 4.0, 6.0)
+
+
+def _quantize_rtn_f64(X: torch.Tensor, fmt: int, had_k: int, four_thirds: bool, static_ts, check: bool):
+    """quantize_rtn of a float64 matrix in the reference's float64 arithmetic, on the device:
+    apply_blockwise (mrfp4_rotate_f64, transforms.py:77-91), absmax / raw / s_T (quantizers.py:
+    170-208), then the float64 encoder of the MSE pass run with the single candidate 1.0 --
+    fp_scale_encode of raw / s_global and u = y / eff rounded onto E2M1 (quantizers.py:157-167,
+    :211-215; formats.py:94-113, :220-262) -- and the metrics of quantizers.py:218-231."""
+    if not bool(torch.isfinite(X).all()):                                  # quantizers.py:99-100
+        if check:
+            raise DataError("non-finite element")
+    M, K = X.shape
+    dev = X.device
+    G = GROUP[fmt]
+    ng = M * K // G
+    L = _lib.lib()
+    with torch.cuda.device(dev):
+        stream = _lib.stream_ptr(torch, dev)
+        Y = torch.empty((M, K), dtype=torch.float64, device=dev)
+        _lib.check(L.mrfp4_rotate_f64(_lib.ptr(X), M, K, X.stride(0), had_k, _lib.ptr(Y), stream))
+        B = Y.view(ng, G)
+        absmax = B.abs().amax(dim=1)
+        raw0 = torch.where(absmax == 0, torch.ones_like(absmax), absmax / 6.0).contiguous()
+        if fmt == FMT_NVFP4:
+            if static_ts is not None:
+                s_global = float(static_ts.item())
+            else:                                                          # quantizers.py:195-200
+                top = float(absmax.max()) / 6.0
+                s_global = float(np.float32(top / 448.0)) if top > 0 else 1.0
+            ts = float(np.float32(s_global))
+        else:
+            s_global, ts = 1.0, float(np.float32(4.0 / 3.0)) if four_thirds else 1.0
+        cand = torch.ones(1, dtype=torch.float64, device=dev)
+        sc = torch.empty(ng, dtype=torch.uint8, device=dev)
+        dec = torch.empty(ng, dtype=torch.float64, device=dev)
+        gerr = torch.empty(ng, dtype=torch.float64, device=dev)
+        res = alloc_result(M, K, fmt, had_k, dev)
+        _lib.check(L.mrfp4_mse_pass(_lib.ptr(Y), ng, fmt, _lib.ptr(cand), 1, _lib.ptr(raw0), s_global, ts,
+                                    _lib.ptr(sc), _lib.ptr(dec), _lib.ptr(gerr), _lib.ptr(res.codes),
+                                    _lib.ptr(res.scratch), stream))
+        _lib.check(L.mrfp4_sf_swizzle(_lib.ptr(sc), _lib.ptr(res.sf), M, K // G, stream))
+        res.tensor_scale_dev.fill_(ts)
+        # metrics (quantizers.py:218-231), rotated domain, float64
+        x2 = float((Y * Y).sum())
+        e2 = float(gerr.sum())
+        arg = B.abs().argmax(dim=1, keepdim=True)                         # first maximum, as np.argmax
+        top = B.gather(1, arg).squeeze(1)
+        c = res.codes.view(ng, G // 2)
+        nib = torch.stack((c & 15, c >> 4), dim=2).view(ng, G).gather(1, arg).squeeze(1).long()
+        mag = torch.tensor(_FP4_MAG, dtype=torch.float64, device=dev)[nib & 7]
+        q = torch.where((nib & 8) != 0, -mag, mag) * (ts * dec)
+        t2 = top * top
+        ratio = torch.where(t2 > 0, (top - q) ** 2 / torch.where(t2 > 0, t2, torch.ones_like(t2)),
+                            torch.zeros_like(t2))
+        res._metrics = (e2 / x2 if x2 > 0 else 0.0, float(ratio.mean()))
     if check:
         res.check()
     return res
@@ -216,6 +330,13 @@ def rotate_f64(X: torch.Tensor, had_k: int) -> torch.Tensor:
     """apply_blockwise (transforms.py:77-91) in float64 on the GPU: the integer Hadamard sums
     are exact (cuBLAS DGEMM of +-1 against bf16 / fp16 / fp32 inputs), then one rounding by
     RN64(1 / RN64(sqrt(k))), the same y = RN64(S * c) the K1 kernels decide on."""
+    if X.dtype == torch.float64:   # the reference's own order (mrfp4_rotate_f64)
+        M, K = X.shape
+        Y = torch.empty((M, K), dtype=torch.float64, device=X.device)
+        with torch.cuda.device(X.device):
+            _lib.check(_lib.lib().mrfp4_rotate_f64(_lib.ptr(X), M, K, X.stride(0), had_k, _lib.ptr(Y),
+                                                   _lib.stream_ptr(torch, X.device)))
+        return Y
     Xd = X.to(torch.float64)
     if not had_k:
         return Xd.contiguous()

@@ -51,6 +51,10 @@ def quantized_linear_sharded(x: torch.Tensor, w_shard: PackedWeight, group=None,
         a = alloc_result(x2.shape[0], x2.shape[1], w_shard.fmt, w_shard.had_k, x2.device)
         act_quant_into(x2, w_shard.fmt, w_shard.had_k, a.codes, a.sf, a.tensor_scale_dev, a.scratch)
         n = w_shard.N
+        # write-after-read: no rank may store into a peer's output while that peer may still be
+        # consuming the previous call's result from it
+        torch.cuda.current_stream(x2.device).synchronize()
+        dist.barrier(group)
         gemm_into_peers(a, w_shard, [po[:, rank * n:(rank + 1) * n] for po in peer_outputs])
         torch.cuda.current_stream(x2.device).synchronize()
         dist.barrier(group)

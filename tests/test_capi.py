@@ -26,7 +26,7 @@ def test_library_exports_every_symbol():
     L = _lib.lib()
     for name in header_symbols():
         assert hasattr(L, name), name
-    assert L.mrfp4_abi_version() == 2
+    assert L.mrfp4_abi_version() == 3
 
 
 def test_gemm_workspace_sizes():
