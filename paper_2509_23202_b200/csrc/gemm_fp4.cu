@@ -481,22 +481,24 @@ __global__ void __launch_bounds__(kThreads, 1)
 // 2-CTA (cta_group::2) kernel: a CTA pair computes a 256 x 256 output tile, persistent
 // over tiles.  K advances in 512-wide stages (two 128-B K slices per row).
 //   warp 0      TMA producer (both CTAs): one 3-D box of 128 rows x 2 slices each for A
-//               and B (cta_group::2: completion bytes counted on the leader's `full`),
-//               this CTA's scale factors (SFA for its 128 rows, SFB for all 256 rows) by
-//               1-D bulk copies into an SF slot (`sf_full`)
+//               and B, and 3-D boxes of this CTA's scale-factor atoms (SFA for its 128
+//               rows, SFB for all 256 rows) -- all cta_group::2, so every byte of both
+//               CTAs is counted on the LEADER's mbarriers (`full` for A/B, `sf_full` for
+//               the SF slot).  Out-of-range boxes (M / N / K tails) are zero-filled by TMA.
 //   warp 1      TMEM allocator (both) + MMA issuer (leader, whole warp converged, one
-//               elected lane issues): 8 x tcgen05.mma.cta_group::2 M=256 N=256 K=64 per
-//               stage, commits multicast to both CTAs (`empty` for the A/B stage,
-//               `tsf_empty` for the TMEM SF slot)
-//   warps 2-5   scale-factor stagers (per CTA, one per TMEM lane quadrant): SMEM -> regs
-//               -> tcgen05.st into a TMEM SF slot, then arrive on the leader's `full`
-//               (tcgen05.cp costs ~16 tensor-pipe cycles per 512-B atom, 24 atoms per
-//               NVFP4 stage -- it would cost ~35% of the MMA time, so it is off the pipe)
-//   warps 6-13  epilogue (per CTA): TMEM -> regs -> * ts_A*ts_W -> bf16 (released to the
+//               elected lane issues): per stage, tcgen05.cp.cta_group::2 copies both CTAs'
+//               SF atoms SMEM -> their own TMEM SF slot, then 8 x tcgen05.mma.cta_group::2
+//               M=256 N=256 K=64 read them; cp and MMA are issued by the same thread, so the
+//               tensor pipe orders them -- no cross-CTA handoff, no cluster-scope fence.
+//               Commits go multicast to both CTAs (`empty` A/B stage, `sf_empty` SF slot).
+//               (scripts/mma2_cp_rate.cu: 12 atom copies per 8 MMAs are free, 24 -- NVFP4 --
+//               cost ~11% when the MMAs are back to back; before this the SF went through
+//               stager warps + a MEMBAR.ALL.GPU per stage on the peer.)
+//   warps 2-9   epilogue (per CTA): TMEM -> regs -> * ts_A*ts_W -> bf16 (released to the
 //               next tile's MMAs before the global stores) / f32 -> global
 // A/B SMEM stages and SF slots are decoupled: 3 A/B stages of 64 KB (~97 B/cycle/SM of
-// TMA throughput measured for this box shape) and 2-3 SF slots, sized so NVFP4's SF
-// (96 TMEM columns per stage) fit next to the 256-column accumulator.
+// TMA throughput measured for this box shape) and 2-3 SF slots (SMEM and TMEM), sized so
+// NVFP4's SF (96 TMEM columns per stage) fit next to the 256-column accumulator.
 // ---------------------------------------------------------------------------
 template <int VEC>
 struct Cfg2 {
@@ -523,8 +525,9 @@ struct Cfg2 {
   static constexpr int kOffBar = kOffSfb + kSfSlots * kSfbBytes;
   static constexpr int kSmem = kOffBar + 512 + 1024;
   static_assert(kSmem <= 232448, "SMEM budget");
-  static constexpr int kThreads2 = 480;   // + warp 14: second peer-SF forwarder
+  static constexpr int kEpiWarp0 = 2;
   static constexpr int kEpiWarps = 8;   // 2 per TMEM lane quadrant, 128 accumulator columns each
+  static constexpr int kThreads2 = 32 * (kEpiWarp0 + kEpiWarps);
 };
 
 // 3-D TMA load (box {128 B, 128 rows, kSlices}) whose completion bytes are counted on the
@@ -661,28 +664,19 @@ struct Ring {
 };
 
 template <int VEC, int OUT, int HKQ = 0>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(480, 1)
-    k_gemm_fp4_2sm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs g) {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<VEC>::kThreads2, 1)
+    k_gemm_fp4_2sm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ CUtensorMap tmSfa, const __grid_constant__ CUtensorMap tmSfb, GemmArgs g) {
   using C = Cfg2<VEC>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kOffBar);   // leader's: A/B landed + SF staged (both CTAs)
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kOffBar);   // leader's: A/B of both CTAs landed
   uint64_t* empty = full + C::kStages;                               // A/B stage free (MMAs committed)
-  uint64_t* sf_full = empty + C::kStages;                            // this CTA's SF landed in SMEM slot
-  uint64_t* sf_empty = sf_full + C::kSfSlots;                        // SF SMEM slot read by the stagers
-  uint64_t* tsf_empty = sf_empty + C::kSfSlots;                      // TMEM SF slot free (MMAs committed)
-  uint64_t* tfull = tsf_empty + C::kSfSlots;
+  uint64_t* sf_full = empty + C::kStages;                            // leader's: SF slot of both CTAs landed
+  uint64_t* sf_empty = sf_full + C::kSfSlots;                        // SF slot (SMEM + TMEM) free
+  uint64_t* tfull = sf_empty + C::kSfSlots;
   uint64_t* tempty = tfull + 1;
-  uint64_t* staged = tempty + 1;                                     // non-leader: its 4 stagers done
-  // NVFP4 hands its scale factors over in two halves (atoms 0-3 for MMAs 0-3, atoms 4-7 for
-  // MMAs 4-7), so the first half can be staged -- and the peer's forwarded -- half a stage
-  // earlier: only 2 TMEM SF slots fit next to the accumulator, and the ~400 ns cluster-scope
-  // release of the peer's handoff otherwise does not fit the one-stage window.
-  constexpr bool kSplit = VEC == 16;
-  uint64_t* staged_b = staged + C::kStages;                          // non-leader: second halves staged
-  uint64_t* sfb_ready = staged_b + C::kStages;                       // leader: second halves staged (both CTAs)
-  uint64_t* tsf_half = sfb_ready + C::kStages;                       // TMEM SF slot's first half free
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tsf_half + C::kSfSlots);
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 1);
 
   const uint32_t rank = sm100::cluster_ctarank();
   const bool leader = rank == 0;
@@ -690,24 +684,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(480, 1)
   // Kernel parameters into registers once (asm "memory" clobbers would force reloads).
   const int num_m_blk = g.num_m_blk, num_kb = g.num_kb, tail_mmas = g.tail_mmas;
   const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
-  const int64_t sf_col_blocks = g.sf_col_blocks, b_row_blocks = g.b_row_blocks, a_row_blocks = (g.M + 127) / 128;
 
   if (warp == 0 && lane == 0) {
     sm100::tma_prefetch_desc(&tmA);
     sm100::tma_prefetch_desc(&tmB);
+    sm100::tma_prefetch_desc(&tmSfa);
+    sm100::tma_prefetch_desc(&tmSfb);
     for (int s = 0; s < C::kStages; ++s) {
-      // leader producer (A/B bytes) + the leader's 4 stager warps + the peer's forwarder
-      sm100::mbar_init(&full[s], 6);
-      sm100::mbar_init(&staged[s], 4);
+      sm100::mbar_init(&full[s], 1);    // the leader producer's expect_tx (bytes of both CTAs)
       sm100::mbar_init(&empty[s], 1);
-      sm100::mbar_init(&staged_b[s], 4);
-      sm100::mbar_init(&sfb_ready[s], 5);   // the leader's 4 stager warps + the peer's forwarder
     }
     for (int s = 0; s < C::kSfSlots; ++s) {
       sm100::mbar_init(&sf_full[s], 1);
-      sm100::mbar_init(&sf_empty[s], 4);  // this CTA's 4 stager warps
-      sm100::mbar_init(&tsf_empty[s], 1);
-      sm100::mbar_init(&tsf_half[s], 1);
+      sm100::mbar_init(&sf_empty[s], 1);
     }
     sm100::mbar_init(tfull, 1);
     sm100::mbar_init(tempty, 2 * C::kEpiWarps);  // epilogue warps x 2 CTAs
@@ -724,128 +713,60 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(480, 1)
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------------------- producer
-      // The weight (B, SFB) does not depend on the act-quant kernel: the first stages'
-      // weight loads are issued BEFORE the PDL wait, so their latency hides behind K1's
-      // tail; A / SFA follow once K1 has completed.
+      // Two independent streams, each bounded by its own ring: A/B codes (3 stages) and scale
+      // factors (2-3 slots); whichever has a free slot is issued next.  The weight (B) of the
+      // first stages does not depend on the act-quant kernel: it is issued BEFORE the PDL
+      // wait, so its latency hides behind K1's tail; A and the scale factors follow.
       Ring ab, sf;
-      WorkIter it(g, cluster, nclusters);
-      Work w;
-      auto sf_bytes = [&](int kb, int m_blk, int n_blk, uint32_t& nat, bool& has_a, int& nb) {
-        const int64_t katom = (int64_t)kb * C::kAtoms;
-        nat = (uint32_t)imin64(C::kAtoms, sf_col_blocks - katom) * 512u;
-        has_a = (int64_t)m_blk * 2 + rank < a_row_blocks;
-        nb = ((int64_t)n_blk * 2 < b_row_blocks) + ((int64_t)n_blk * 2 + 1 < b_row_blocks);
+      StageIter abq(g, cluster, nclusters, num_m_blk), sfq(g, cluster, nclusters, num_m_blk);
+      auto arm = [&](uint64_t* bar, uint32_t bytes) {
+        if (leader) sm100::mbar_arrive_expect_tx(bar, 2u * bytes);   // this CTA's and the peer's bytes
       };
-      // A stager arrives on full[t % kStages] only after its TMEM SF slot was freed by the MMAs
-      // of stage t - kSfSlots, i.e. after phase t - kStages of that barrier completed.
-      static_assert(C::kSfSlots <= C::kStages, "SF run-ahead must not lap the A/B ring");
-      StageIter sfq(g, cluster, nclusters, num_m_blk);
-      auto issue_next_sf = [&] {
-        if (!sfq.live) return;
-        sm100::mbar_wait(&sf_empty[sf.idx], sf.ph ^ 1);
-        uint32_t nat;
-        bool has_a;
-        int nbk;
+      auto load_ab = [&](bool a_part, bool b_part) {
+        const int kb = abq.kb, mb = abq.m_blk(), nb = abq.n_blk();
+        const uint32_t bar = sm100::leader_bar(&full[ab.idx]);
+        if (b_part)
+          tma_load_3d_2sm(smem + C::kOffB + ab.idx * C::kBBytes, &tmB, bar, nb * 256 + (int)rank * 128,
+                          kb * C::kSlices);
+        if (a_part)
+          tma_load_3d_2sm(smem + C::kOffA + ab.idx * C::kABytes, &tmA, bar, mb * 256 + (int)rank * 128,
+                          kb * C::kSlices);
+      };
+      auto load_sf = [&] {
         const int kb = sfq.kb, mb = sfq.m_blk(), nb = sfq.n_blk();
-        sf_bytes(kb, mb, nb, nat, has_a, nbk);
-        sm100::mbar_arrive_expect_tx(&sf_full[sf.idx], (has_a ? nat : 0u) + nat * (uint32_t)nbk);
-        const int64_t katom = (int64_t)kb * C::kAtoms;
-        const int64_t ra = (int64_t)mb * 2 + rank, rb0 = (int64_t)nb * 2;
-        if (has_a)
-          sm100::bulk_load(smem + C::kOffSfa + sf.idx * C::kSfaBytes, g.a_sf + (ra * sf_col_blocks + katom) * 512,
-                           nat, &sf_full[sf.idx]);
-#pragma unroll
-        for (int j = 0; j < 2; ++j)
-          if (rb0 + j < b_row_blocks)
-            sm100::bulk_load(smem + C::kOffSfb + sf.idx * C::kSfbBytes + j * C::kSfaBytes,
-                             g.b_sf + ((rb0 + j) * sf_col_blocks + katom) * 512, nat, &sf_full[sf.idx]);
+        arm(&sf_full[sf.idx], C::kSfaBytes + C::kSfbBytes);
+        const uint32_t bar = sm100::leader_bar(&sf_full[sf.idx]);
+        // SF boxes {256 B, 2 * kAtoms half-atoms, 1 | 2 row blocks}: this CTA's 128 rows of A,
+        // both 128-row blocks of the tile's B (each CTA's MMA half needs all 256 N columns).
+        tma_load_3d_2sm(smem + C::kOffSfa + sf.idx * C::kSfaBytes, &tmSfa, bar, 2 * C::kAtoms * kb, mb * 2 + (int)rank);
+        tma_load_3d_2sm(smem + C::kOffSfb + sf.idx * C::kSfbBytes, &tmSfb, bar, 2 * C::kAtoms * kb, nb * 2);
         sfq.advance();
         sf.next<C::kSfSlots>();
       };
-      auto load_a_codes = [&](int kb, int m_blk, int abi) {
-        tma_load_3d_2sm(smem + C::kOffA + abi * C::kABytes, &tmA, sm100::leader_bar(&full[abi]),
-                        m_blk * 256 + (int)rank * 128, kb * C::kSlices);
-      };
-      auto load_b_codes = [&](int kb, int n_blk, int abi) {
-        tma_load_3d_2sm(smem + C::kOffB + abi * C::kBBytes, &tmB, sm100::leader_bar(&full[abi]),
-                        n_blk * 256 + (int)rank * 128, kb * C::kSlices);
-      };
-      auto arm_ab = [&](int abi) {
-        if (leader) sm100::mbar_arrive_expect_tx(&full[abi], 2u * (C::kABytes + C::kBBytes));
-      };
-      // Scale factors run ahead of the A/B codes (SF of stage t is issued right after the A/B of
-      // stage t - ahead): the peer CTA's scale factors then reach the leader through the
-      // cluster-scope release (forwarder below) before the MMAs of stage t are due
-      // (scripts/ahead_probe.py).
-      // MXFP4 (3 SF slots, 2 forwarders) runs two stages ahead: c1 56.1 -> 53.4 us, 70B down
-      // 191.7 -> 180.5; NVFP4 (2 slots) is best at one (223.8 vs 229.7 at two).
-      constexpr int ahead = VEC == 32 ? 2 : 1;
+      // PDL pre-issue: the weight half of the first A/B stages
       int pre = 0;
-      if (it.next(g, w)) {
-        const int m_blk = w.tile % num_m_blk, n_blk = w.tile / num_m_blk;
-        pre = g.preissue ? min(C::kStages, w.kb1 - w.kb0) : 0;
-        for (int s2 = 0; s2 < pre; ++s2) {
-          arm_ab(s2);
-          load_b_codes(w.kb0 + s2, n_blk, s2);
+      if (g.preissue) {
+        StageIter q2 = abq;
+        for (; pre < C::kStages && q2.live; ++pre) {
+          arm(&full[pre], C::kABytes + C::kBBytes);
+          tma_load_3d_2sm(smem + C::kOffB + pre * C::kBBytes, &tmB, sm100::leader_bar(&full[pre]),
+                          q2.n_blk() * 256 + (int)rank * 128, q2.kb * C::kSlices);
+          q2.advance();
         }
-        pdl_wait();
-        for (int s2 = 0; s2 < ahead; ++s2) issue_next_sf();
-        for (int s2 = 0; s2 < pre; ++s2) {
-          load_a_codes(w.kb0 + s2, m_blk, s2);
-          ab.next<C::kStages>();
-          issue_next_sf();
-        }
-        bool more = true;
-        while (more) {
-          const int mb = w.tile % num_m_blk, nb = w.tile / num_m_blk;
-          for (int kb = w.kb0 + pre; kb < w.kb1; ++kb) {
-            sm100::mbar_wait(&empty[ab.idx], ab.ph ^ 1);
-            arm_ab(ab.idx);
-            load_a_codes(kb, mb, ab.idx);
-            load_b_codes(kb, nb, ab.idx);
-            ab.next<C::kStages>();
-            issue_next_sf();
-          }
-          pre = 0;
-          more = it.next(g, w);
-        }
-        while (sfq.live) issue_next_sf();
-      } else {
-        pdl_wait();
       }
-    }
-  } else if ((warp == 1 || warp == 14) && !leader) {
-    // ------------------------------------------------- peer SF forwarder (non-leader)
-    // The leader's MMAs read this CTA's scale factors from this CTA's TMEM.  Ordering those
-    // tcgen05.st before the MMAs needs a CLUSTER-scope release: with a cta-scope one the MMAs
-    // measurably read stale scale factors (whole 32-row quadrants of the peer's rows wrong,
-    // 8192 x 16384 -> 53248, tests/test_gpu_fullsize.py).  A cluster-scope release is a
-    // MEMBAR.ALL.GPU, so one thread pays it per stage here, off the stager warps' path: it
-    // collects the 4 local stager arrivals and forwards one arrival to the leader's `full`.
-    // Two forwarders (warps 1 and 14) take alternate stages, so a slow membar under heavy
-    // memory traffic does not queue the next stage behind it.
-    if (lane == 0) {
-      Ring ab;
-      WorkIter it(g, cluster, nclusters);
-      Work w;
-      int st = 0;
-      // MXFP4: the two forwarders take alternate stages (c2-down 200 -> 188 us).  NVFP4: warp 1
-      // forwards every stage's first half, warp 14 every second half.
-      const int mine = warp == 1 ? 0 : 1;
-      while (it.next(g, w)) {
-        for (int kb = w.kb0; kb < w.kb1; ++kb, ++st) {
-          if constexpr (kSplit) {
-            if (mine == 0) {
-              sm100::mbar_wait(&staged[ab.idx], ab.ph);
-              sm100::mbar_arrive_remote(&full[ab.idx], 0);
-            } else {
-              sm100::mbar_wait(&staged_b[ab.idx], ab.ph);
-              sm100::mbar_arrive_remote(&sfb_ready[ab.idx], 0);
-            }
-          } else if ((st & 1) == mine) {
-            sm100::mbar_wait(&staged[ab.idx], ab.ph);
-            sm100::mbar_arrive_remote(&full[ab.idx], 0);
-          }
+      pdl_wait();
+      for (int i = 0; i < pre; ++i) {   // A of the pre-issued stages (their slots were never used)
+        load_ab(true, false);
+        abq.advance();
+        ab.next<C::kStages>();
+      }
+      while (abq.live || sfq.live) {
+        if (sfq.live && sm100::mbar_test(&sf_empty[sf.idx], sf.ph ^ 1)) {
+          load_sf();
+        } else if (abq.live && sm100::mbar_test(&empty[ab.idx], ab.ph ^ 1)) {
+          arm(&full[ab.idx], C::kABytes + C::kBBytes);
+          load_ab(true, true);
+          abq.advance();
           ab.next<C::kStages>();
         }
       }
@@ -854,129 +775,48 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(480, 1)
     if (leader) {
       // ---------------------------------------------------------- MMA issuer
       // The whole warp runs the loop (converged, uniform descriptors); one elected lane
-      // issues.  A stage's 8 MMAs (~1000 cycles of tensor work) are queued before the
-      // thread waits for the next stage, so barrier latency never starves the pipe.
+      // issues.  A stage's SF copies and 8 MMAs (~1000 cycles of tensor work) are queued
+      // before the thread waits for the next stage, so barrier latency never starves the pipe.
+      // An SF slot's TMEM columns are rewritten only after sf_full of its next use, which the
+      // producer arms only after sf_empty (the previous use's MMAs completed).
       const uint32_t el = sm100::elect_lane();
       Ring ab, sf;
       uint32_t acc_phase = 0;
       const uint64_t adesc0 = sm100::smem_desc(sm100::smem_u32(smem + C::kOffA), 16, 1024, 2);
       const uint64_t bdesc0 = sm100::smem_desc(sm100::smem_u32(smem + C::kOffB), 16, 1024, 2);
+      const uint32_t sfa_s0 = sm100::smem_u32(smem + C::kOffSfa), sfb_s0 = sm100::smem_u32(smem + C::kOffSfb);
       const uint32_t sf0 = tmem_base + C::kAccCols;
-      unsigned long long* dbg = (g.dbg && cluster == 0) ? g.dbg : nullptr;  // perf traces (tests pass null)
-      int ntl = 0;
       WorkIter it(g, cluster, nclusters);
       Work w;
-      for (; it.next(g, w); ++ntl) {
-        if (dbg && ntl < 4) dbg[ntl * 260] = clock64();
+      while (it.next(g, w)) {
         sm100::mbar_wait_cluster(tempty, acc_phase ^ 1);   // both CTAs' epilogues (remote arrivals)
-        if (dbg && ntl < 4) dbg[ntl * 260 + 1] = clock64();
         for (int kb = w.kb0; kb < w.kb1; ++kb) {
+          sm100::mbar_wait(&sf_full[sf.idx], sf.ph);
           sm100::mbar_wait(&full[ab.idx], ab.ph);
-          if (dbg && ntl < 4 && kb - w.kb0 < 128) dbg[ntl * 260 + 2 + 2 * (kb - w.kb0)] = clock64();
           sm100::tc_fence_after();
           const uint32_t sfa_t = sf0 + sf.idx * C::kSfCols, sfb_t = sfa_t + C::kSfaCols;
+          const uint32_t sfa_s = sfa_s0 + sf.idx * C::kSfaBytes, sfb_s = sfb_s0 + sf.idx * C::kSfbBytes;
+#pragma unroll
+          for (int a = 0; a < C::kAtoms; ++a) {   // TMEM SFB order: atom-major, then 128-row block
+            sm100::tc_cp_32x128b_warpx4_2sm_if(el, sfa_t + a * 4, sm100::smem_desc(sfa_s + a * 512, 0, 128, 0));
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+              sm100::tc_cp_32x128b_warpx4_2sm_if(el, sfb_t + (2 * a + j) * 4,
+                                                 sm100::smem_desc(sfb_s + (j * C::kAtoms + a) * 512, 0, 128, 0));
+          }
           const uint64_t ad = desc_add(adesc0, (uint32_t)(ab.idx * (C::kABytes >> 4)));
           const uint64_t bd = desc_add(bdesc0, (uint32_t)(ab.idx * (C::kBBytes >> 4)));
-          if constexpr (kSplit) {
-            const int nk = (kb + 1 < num_kb || tail_mmas == 0) ? C::kMmas : tail_mmas;
-            if (nk >= 4) issue_stage_mmas<VEC, 0, 4>(el, tmem_base, ad, bd, sfa_t, sfb_t, kb == w.kb0);
-            else issue_stage_tail<VEC>(nk, el, tmem_base, ad, bd, sfa_t, sfb_t, kb == w.kb0);
-            sm100::tc_commit_2sm_mc_if(el, &tsf_half[sf.idx], 0x3);
-            sm100::mbar_wait(&sfb_ready[ab.idx], ab.ph);   // second halves of both CTAs staged
-            sm100::tc_fence_after();
-            switch (nk) {
-              case 5: issue_stage_mmas<VEC, 4, 5>(el, tmem_base, ad, bd, sfa_t, sfb_t, false); break;
-              case 6: issue_stage_mmas<VEC, 4, 6>(el, tmem_base, ad, bd, sfa_t, sfb_t, false); break;
-              case 7: issue_stage_mmas<VEC, 4, 7>(el, tmem_base, ad, bd, sfa_t, sfb_t, false); break;
-              case 8: issue_stage_mmas<VEC, 4, 8>(el, tmem_base, ad, bd, sfa_t, sfb_t, false); break;
-              default: break;
-            }
-          } else {
-            if (kb + 1 < num_kb || tail_mmas == 0)
-              issue_stage_mmas<VEC, 0, C::kMmas>(el, tmem_base, ad, bd, sfa_t, sfb_t, kb == w.kb0);
-            else
-              issue_stage_tail<VEC>(tail_mmas, el, tmem_base, ad, bd, sfa_t, sfb_t, kb == w.kb0);
-          }
+          if (kb + 1 < num_kb || tail_mmas == 0)
+            issue_stage_mmas<VEC, 0, C::kMmas>(el, tmem_base, ad, bd, sfa_t, sfb_t, kb == w.kb0);
+          else
+            issue_stage_tail<VEC>(tail_mmas, el, tmem_base, ad, bd, sfa_t, sfb_t, kb == w.kb0);
           sm100::tc_commit_2sm_mc_if(el, &empty[ab.idx], 0x3);
-          sm100::tc_commit_2sm_mc_if(el, &tsf_empty[sf.idx], 0x3);
-          if (dbg && ntl < 4 && kb - w.kb0 < 128) dbg[ntl * 260 + 3 + 2 * (kb - w.kb0)] = clock64();
+          sm100::tc_commit_2sm_mc_if(el, &sf_empty[sf.idx], 0x3);
           ab.next<C::kStages>();
           sf.next<C::kSfSlots>();
         }
         sm100::tc_commit_2sm_mc_if(el, tfull, 0x3);
         acc_phase ^= 1;
-      }
-    }
-  } else if (warp == 14) {
-    // leader CTA: no role for the second forwarder warp
-  } else if (warp < 6) {
-    // ------------------------------------------ scale-factor stagers (both CTAs)
-    // TMEM slot layout (replicated over the 4 lane quadrants, as tcgen05.cp.warpx4
-    // would produce): lane 32q+l, column c+j of a 128-row atom holds the 4 scale
-    // codes of row l+32j -- i.e. bytes [16l, 16l+16) of the 512-B SMEM atom.
-    const int q = warp & 3;
-    Ring ab, sf;
-    const uint32_t sa0 = sm100::smem_u32(smem + C::kOffSfa) + lane * 16, sb0 = sm100::smem_u32(smem + C::kOffSfb) + lane * 16;
-    WorkIter it(g, cluster, nclusters);
-    Work w;
-    while (it.next(g, w)) {
-      for (int kb = w.kb0; kb < w.kb1; ++kb) {
-        sm100::mbar_wait(&sf_full[sf.idx], sf.ph);
-        const uint32_t sa = sa0 + sf.idx * C::kSfaBytes, sb = sb0 + sf.idx * C::kSfbBytes;
-        uint32_t ra[C::kSfaCols], rb[C::kSfbCols];
-#pragma unroll
-        for (int a = 0; a < C::kAtoms; ++a) {
-          const uint4 va = sm100::lds128(sa + a * 512);
-          ra[4 * a + 0] = va.x; ra[4 * a + 1] = va.y; ra[4 * a + 2] = va.z; ra[4 * a + 3] = va.w;
-#pragma unroll
-          for (int j = 0; j < 2; ++j) {  // TMEM order: atom-major, then 128-row block
-            const uint4 vb = sm100::lds128(sb + (j * C::kAtoms + a) * 512);
-            rb[8 * a + 4 * j + 0] = vb.x; rb[8 * a + 4 * j + 1] = vb.y;
-            rb[8 * a + 4 * j + 2] = vb.z; rb[8 * a + 4 * j + 3] = vb.w;
-          }
-        }
-        const uint32_t t0 = tmem_base + ((uint32_t)(q * 32) << 16) + C::kAccCols + sf.idx * C::kSfCols;
-        if constexpr (kSplit) {
-          // first half: SFA columns [0, 16) and SFB columns [0, 32) (atoms 0-3, MMAs 0-3)
-          sm100::mbar_wait(&tsf_half[sf.idx], sf.ph ^ 1);        // previous use's MMAs 0-3 done
-          sm100::tc_fence_after();
-          sm100::tmem_st_32x32b<16>(t0, ra);
-          sm100::tmem_st_32x32b<16>(t0 + C::kSfaCols, rb);
-          sm100::tmem_st_32x32b<16>(t0 + C::kSfaCols + 16, rb + 16);
-          sm100::tmem_st_wait();
-          sm100::tc_fence_before();
-          __syncwarp();
-          if (lane == 0) sm100::mbar_arrive(leader ? &full[ab.idx] : &staged[ab.idx]);
-          sm100::mbar_wait(&tsf_empty[sf.idx], sf.ph ^ 1);       // previous use's MMAs 4-7 done
-          sm100::tc_fence_after();
-          sm100::tmem_st_32x32b<16>(t0 + 16, ra + 16);
-          sm100::tmem_st_32x32b<16>(t0 + C::kSfaCols + 32, rb + 32);
-          sm100::tmem_st_32x32b<16>(t0 + C::kSfaCols + 48, rb + 48);
-          sm100::tmem_st_wait();
-          sm100::tc_fence_before();
-          __syncwarp();
-          if (lane == 0) sm100::mbar_arrive(&sf_empty[sf.idx]);
-          if (lane == 0) sm100::mbar_arrive(leader ? &sfb_ready[ab.idx] : &staged_b[ab.idx]);
-          ab.next<C::kStages>();
-          sf.next<C::kSfSlots>();
-          continue;
-        }
-        sm100::mbar_wait(&tsf_empty[sf.idx], sf.ph ^ 1);        // TMEM slot's previous MMAs done
-        sm100::tc_fence_after();
-#pragma unroll
-        for (int c = 0; c < C::kSfaCols; c += 16) sm100::tmem_st_32x32b<16>(t0 + c, ra + c);
-#pragma unroll
-        for (int c = 0; c < C::kSfbCols; c += 16) sm100::tmem_st_32x32b<16>(t0 + C::kSfaCols + c, rb + c);
-        sm100::tmem_st_wait();
-        sm100::tc_fence_before();
-        __syncwarp();
-        // The SMEM slot is released only once its values have been consumed (stored to TMEM):
-        // with the scale factors issued ahead of the A/B codes the producer refills a freed slot
-        // at once, and an arrival right after the 16-B shared loads let that refill race them.
-        if (lane == 0) sm100::mbar_arrive(&sf_empty[sf.idx]);
-        if (lane == 0) sm100::mbar_arrive(leader ? &full[ab.idx] : &staged[ab.idx]);
-        ab.next<C::kStages>();
-        sf.next<C::kSfSlots>();
       }
     }
   } else {
@@ -985,7 +825,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(480, 1)
     // bf16 output: the 128 columns are pulled into registers (as bf16 pairs) and the
     // accumulator is released BEFORE the global stores, so the next tile's MMAs start
     // while this tile's output is being written.
-    const int q = warp & 3, h = (warp - 6) >> 2;
+    const int q = warp & 3, h = (warp - C::kEpiWarp0) >> 2;
     pdl_wait();
     const float alpha = __ldg(g.a_ts) * __ldg(g.b_ts);
     if constexpr (OUT == kOutMxq)
@@ -1116,6 +956,23 @@ bool make_code_map3(CUtensorMap* tm, const uint8_t* ptr, int64_t rows, int64_t K
   return r == CUDA_SUCCESS;
 }
 
+// Swizzled scale factors [row_blocks][col_blocks atoms of 512 B] viewed as 3-D
+// {256 B, 2 * col_blocks half-atoms, row_blocks}: a box {256, 2 * atoms, nrb} is `atoms`
+// consecutive K atoms of `nrb` consecutive 128-row blocks (row blocks / atoms past the end
+// are zero-filled, and still counted as transaction bytes).
+bool make_sf_map(CUtensorMap* tm, const uint8_t* ptr, int64_t row_blocks, int64_t col_blocks, int atoms, int nrb) {
+  auto encode = get_encode_fn();
+  if (!encode) return false;
+  cuuint64_t dims[3] = {256, (cuuint64_t)(2 * col_blocks), (cuuint64_t)row_blocks};
+  cuuint64_t strides[2] = {256, (cuuint64_t)(col_blocks * 512)};
+  cuuint32_t box[3] = {256, (cuuint32_t)(2 * atoms), (cuuint32_t)nrb};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = encode(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(ptr), dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 // Split-K plan for `tiles` output tiles of `num_kb` k-blocks: about one unit per SM, at
 // least 2 k-blocks per split.
 void splitk_plan(int tiles, int num_kb, int* splits, int* kb_per);
@@ -1174,9 +1031,11 @@ int launch2(const uint8_t* a, const uint8_t* b, const GemmArgs& args0, cudaStrea
       }) < 0)
     return MRFP4_ECUDA;
   GemmArgs g = args0;
-  CUtensorMap tmA, tmB;
+  CUtensorMap tmA, tmB, tmSfa, tmSfb;
   const int64_t sfc = g.K / VEC;
-  if (!make_code_map3(&tmA, a, g.M, g.K, 128, C::kSlices) || !make_code_map3(&tmB, b, g.N, g.K, 128, C::kSlices))
+  if (!make_code_map3(&tmA, a, g.M, g.K, 128, C::kSlices) || !make_code_map3(&tmB, b, g.N, g.K, 128, C::kSlices) ||
+      !make_sf_map(&tmSfa, g.a_sf, ceil_div(g.M, 128), ceil_div(sfc, 4), C::kAtoms, 1) ||
+      !make_sf_map(&tmSfb, g.b_sf, ceil_div(g.N, 128), ceil_div(sfc, 4), C::kAtoms, 2))
     return MRFP4_ECUDA;
   g.num_m_blk = (int)ceil_div(g.M, 256);
   g.num_n_blk = (int)ceil_div(g.N, 256);
@@ -1187,7 +1046,8 @@ int launch2(const uint8_t* a, const uint8_t* b, const GemmArgs& args0, cudaStrea
   const int tiles = g.num_m_blk * g.num_n_blk;
   int nclu = std::min(tiles, num_sms() / 2);
   if (g_force_grid > 0) nclu = std::min(nclu, std::max(1, g_force_grid / 2));
-  return launch_pdl(k_gemm_fp4_2sm<VEC, OUT, HKQ>, dim3(2 * nclu), dim3(C::kThreads2), C::kSmem, s, tmA, tmB, g) ==
+  return launch_pdl(k_gemm_fp4_2sm<VEC, OUT, HKQ>, dim3(2 * nclu), dim3(C::kThreads2), C::kSmem, s, tmA, tmB, tmSfa,
+                    tmSfb, g) ==
                  cudaSuccess
              ? MRFP4_OK
              : MRFP4_ECUDA;

@@ -40,6 +40,18 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
       "r"(parity), "r"(1000000u)
       : "memory");
 }
+// Non-blocking: has the phase with `parity` completed?
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t r;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.b32 %0, 1, 0, P1;\n\t}"
+      : "=r"(r)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return r != 0;
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
   asm volatile(
@@ -219,6 +231,14 @@ __device__ __forceinline__ void tmem_dealloc_2sm(uint32_t taddr, uint32_t ncols)
 }
 __device__ __forceinline__ void tc_cp_32x128b_warpx4_2sm(uint32_t taddr, uint64_t sdesc) {
   asm volatile("tcgen05.cp.cta_group::2.32x128b.warpx4 [%0], %1;" ::"r"(taddr), "l"(sdesc) : "memory");
+}
+// Warp-converged form (see tc_mma_fp4_2sm_if): only the lane with `leader_lane` set issues.
+__device__ __forceinline__ void tc_cp_32x128b_warpx4_2sm_if(uint32_t leader_lane, uint32_t taddr, uint64_t sdesc) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\tsetp.ne.b32 e, %2, 0;\n\t"
+      "@e tcgen05.cp.cta_group::2.32x128b.warpx4 [%0], %1;\n\t}" ::"r"(taddr),
+      "l"(sdesc), "r"(leader_lane)
+      : "memory");
 }
 // Commit to the same-offset mbarrier in every CTA of `mask` (multicast within the cluster).
 __device__ __forceinline__ void tc_commit_2sm_mc(uint64_t* bar, uint16_t mask) {
