@@ -14,7 +14,8 @@ import threading
 from .errors import DataError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmrfp4.so")
+# MRFP4_LIB: an alternative build of the same library (perf experiments, e.g. the MRFP4_TRACE build)
+LIB_PATH = os.environ.get("MRFP4_LIB") or os.path.join(_HERE, "libmrfp4.so")
 
 OK, EINVAL, EUNSUPPORTED, ECUDA = 0, 1, 2, 3
 DT_BF16, DT_F16, DT_F32, DT_F64 = 0, 1, 2, 3

@@ -788,11 +788,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<VEC>::kThreads2
       const uint32_t sf0 = tmem_base + C::kAccCols;
       WorkIter it(g, cluster, nclusters);
       Work w;
+#ifdef MRFP4_TRACE
+      // perf experiments (scripts/k2_timeline.py): per-stage clock64 of cluster 0's MMA thread
+      unsigned long long* tr = (g.dbg && cluster == 0 && lane == 0) ? g.dbg : nullptr;
+      int tn = 0;
+      auto stamp = [&](int tag) { if (tr && tn < 8192) { tr[2 * tn] = clock64(); tr[2 * tn + 1] = tag; ++tn; } };
+#else
+      auto stamp = [](int) {};
+#endif
       while (it.next(g, w)) {
+        stamp(0);
         sm100::mbar_wait_cluster(tempty, acc_phase ^ 1);   // both CTAs' epilogues (remote arrivals)
+        stamp(1);
         for (int kb = w.kb0; kb < w.kb1; ++kb) {
           sm100::mbar_wait(&sf_full[sf.idx], sf.ph);
+          stamp(2);
           sm100::mbar_wait(&full[ab.idx], ab.ph);
+          stamp(3);
           sm100::tc_fence_after();
           const uint32_t sfa_t = sf0 + sf.idx * C::kSfCols, sfb_t = sfa_t + C::kSfaCols;
           const uint32_t sfa_s = sfa_s0 + sf.idx * C::kSfaBytes, sfb_s = sfb_s0 + sf.idx * C::kSfbBytes;
@@ -806,12 +818,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<VEC>::kThreads2
           }
           const uint64_t ad = desc_add(adesc0, (uint32_t)(ab.idx * (C::kABytes >> 4)));
           const uint64_t bd = desc_add(bdesc0, (uint32_t)(ab.idx * (C::kBBytes >> 4)));
+#ifdef MRFP4_TRACE
+          if (g.debug == 2) {   // load pipeline only: no MMA (commits arrive at once)
+          } else
+#endif
           if (kb + 1 < num_kb || tail_mmas == 0)
             issue_stage_mmas<VEC, 0, C::kMmas>(el, tmem_base, ad, bd, sfa_t, sfb_t, kb == w.kb0);
           else
             issue_stage_tail<VEC>(tail_mmas, el, tmem_base, ad, bd, sfa_t, sfb_t, kb == w.kb0);
           sm100::tc_commit_2sm_mc_if(el, &empty[ab.idx], 0x3);
           sm100::tc_commit_2sm_mc_if(el, &sf_empty[sf.idx], 0x3);
+          stamp(4);
           ab.next<C::kStages>();
           sf.next<C::kSfSlots>();
         }
