@@ -187,13 +187,24 @@ int mrfp4_gemm_peers(const uint8_t* a, const uint8_t* a_sf, const float* a_ts, c
  * quantize_rtn(Y, FormatSpec.mxfp4(), transform=hadamard(next_had_k)) (quantizers.py:247-255)
  * -- E2M1 codes [M, N/2], swizzled E8M0 scales [M, N/32] (padding rows zeroed) and the tensor
  * scale f32(4/3) -- bit-identical to mrfp4_act_quant on Y.  y_bf16 may be NULL (Y not stored).
- * Requires M > 128, K % 256 == 0, N % 128 == 0, next_had_k in {0, 16, 32}; status: bit 1 =
- * non-finite Y.  MXFP4 only: NVFP4's tensor scale needs the whole Y before any group is encoded.
+ * Requires M > 128, K % 256 == 0, N % 128 == 0, next_had_k in {0, 16, 32, 64, 128}; status: bit 1 =
+ * non-finite Y.  A whole-Y NVFP4 tensor scale cannot be fused (it needs all of Y before any group
+ * is encoded): mrfp4_gemm_quant_next_ex takes a static one.
  */
 int mrfp4_gemm_quant_next(const uint8_t* a, const uint8_t* a_sf, const float* a_ts, const uint8_t* b,
                           const uint8_t* b_sf, const float* b_ts, void* y_bf16, int64_t ldy, int64_t M, int64_t N,
                           int64_t K, int fmt, int next_had_k, uint8_t* next_codes, uint8_t* next_sf,
                           float* next_tensor_scale, uint32_t* status, void* stream);
+/* The same for either next-layer format: next_fmt MXFP4 (as above), or NVFP4 against the given
+ * device global scale next_static_ts (a static / calibrated s_T, see mrfp4_act_quant_opts) --
+ * identical to mrfp4_act_quant_ex on Y with opts.nv_tensor_scale = next_static_ts.  next_had_k in
+ * {0, 16, 32, 64, 128} (64 / 128: the cross-segment stages run in the epilogue thread, which
+ * holds 128 consecutive output columns).  next_sf: scale codes [M, N/G] (G = 16 or 32). */
+int mrfp4_gemm_quant_next_ex(const uint8_t* a, const uint8_t* a_sf, const float* a_ts, const uint8_t* b,
+                             const uint8_t* b_sf, const float* b_ts, void* y_bf16, int64_t ldy, int64_t M, int64_t N,
+                             int64_t K, int fmt, int next_fmt, int next_had_k, const float* next_static_ts,
+                             uint8_t* next_codes, uint8_t* next_sf, float* next_tensor_scale, uint32_t* status,
+                             void* stream);
 
 /*
  * Offline MSE scale search (replaces the numpy loops of

@@ -49,6 +49,8 @@ SIGNATURES = {
     "mrfp4_dequantize": (_int, [_vp, _vp, _vp, _i64, _i64, _int, _vp, _vp]),
     "mrfp4_gemm_quant_next": (_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _int, _int, _vp, _vp,
                                      _vp, _vp, _vp]),
+    "mrfp4_gemm_quant_next_ex": (_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _int, _int, _int,
+                                        _vp, _vp, _vp, _vp, _vp, _vp]),
     "mrfp4_mse_pass": (_int, [_vp, _i64, _int, _vp, _int, _vp, _c.c_double, _c.c_double, _vp, _vp, _vp, _vp, _vp,
                               _vp]),
     "mrfp4_mse_group_err": (_int, [_vp, _i64, _int, _vp, _c.c_double, _vp, _vp, _vp]),

@@ -422,25 +422,6 @@ __device__ __forceinline__ void zero_sf_padding(const AQParams& p) {
   }
 }
 
-// Per-launch encode constants.  MXFP4: ts = f32(4/3) (quantizers.py:34,191).  NVFP4: derived
-// from the whole-tensor max exactly as numpy does (quantizers.py:187, :198-200).
-struct EncConsts {
-  float st32 = 1.33333337306976318359375f;
-  double st64 = 1.0;
-  float kenc = 0.f, knv = 0.f;
-  uint32_t zero_code = 0;
-};
-
-__device__ __forceinline__ EncConsts nv_consts_st(const AQParams& p, float st32) {
-  EncConsts k;
-  k.st32 = st32;
-  k.st64 = (double)k.st32;
-  k.zero_code = e4m3_rne64(1.0 / k.st64);                               // raw = 1.0 sentinel
-  k.kenc = __double2float_rn(p.c64 / 6.0 / k.st64);
-  k.knv = __double2float_rn(p.c64 / k.st64);
-  return k;
-}
-
 __device__ __forceinline__ EncConsts nv_consts(const AQParams& p, uint32_t gmax_bits) {
   const double top = (double)__uint_as_float(gmax_bits) * p.c64 / 6.0;  // absmax.max() / FP4_MAX
   return nv_consts_st(p, top > 0.0 ? __double2float_rn(top / 448.0) : 1.0f);   // f32(top / E4M3 max)

@@ -27,8 +27,8 @@ int launch_dequantize(const uint8_t* codes, const uint8_t* sf, const float* ts, 
                       float* out, cudaStream_t s);
 int launch_gemm_quant_next(const uint8_t* a, const uint8_t* a_sf, const float* a_ts, const uint8_t* b,
                            const uint8_t* b_sf, const float* b_ts, void* y, int64_t ldy, int64_t M, int64_t N,
-                           int64_t K, int fmt, int next_hk, uint8_t* q_codes, uint8_t* q_sf, float* q_ts,
-                           uint32_t* q_status, cudaStream_t s);
+                           int64_t K, int fmt, int next_fmt, int next_hk, const float* next_static_ts,
+                           uint8_t* q_codes, uint8_t* q_sf, float* q_ts, uint32_t* q_status, cudaStream_t s);
 int launch_gemm_peers(const uint8_t* a, const uint8_t* a_sf, const float* a_ts, const uint8_t* b,
                       const uint8_t* b_sf, const float* b_ts, void* const* dsts, int ndst, int64_t M, int64_t N,
                       int64_t K, int64_t ldd, int fmt, cudaStream_t s);
@@ -237,21 +237,34 @@ int mrfp4_gemm_quant_next(const uint8_t* a, const uint8_t* a_sf, const float* a_
                           const uint8_t* b_sf, const float* b_ts, void* y_bf16, int64_t ldy, int64_t M, int64_t N,
                           int64_t K, int fmt, int next_had_k, uint8_t* next_codes, uint8_t* next_sf,
                           float* next_tensor_scale, uint32_t* status, void* stream) {
+  return mrfp4_gemm_quant_next_ex(a, a_sf, a_ts, b, b_sf, b_ts, y_bf16, ldy, M, N, K, fmt, MRFP4_FMT_MXFP4,
+                                  next_had_k, nullptr, next_codes, next_sf, next_tensor_scale, status, stream);
+}
+
+int mrfp4_gemm_quant_next_ex(const uint8_t* a, const uint8_t* a_sf, const float* a_ts, const uint8_t* b,
+                             const uint8_t* b_sf, const float* b_ts, void* y_bf16, int64_t ldy, int64_t M, int64_t N,
+                             int64_t K, int fmt, int next_fmt, int next_had_k, const float* next_static_ts,
+                             uint8_t* next_codes, uint8_t* next_sf, float* next_tensor_scale, uint32_t* status,
+                             void* stream) {
   if (mrfp4_group_size(fmt) == 0) return fail(MRFP4_EUNSUPPORTED, "unknown format %d", fmt);
+  if (mrfp4_group_size(next_fmt) == 0) return fail(MRFP4_EUNSUPPORTED, "unknown next-layer format %d", next_fmt);
   if (M < 1 || N < 1 || K < 1) return fail(MRFP4_EINVAL, "empty GEMM");
   if (M <= 128 || K % 256)
     return fail(MRFP4_EUNSUPPORTED, "fused next-layer quantization needs M > 128 and K %% 256 == 0 (2-CTA GEMM)");
   if (N % 128) return fail(MRFP4_EUNSUPPORTED, "fused next-layer quantization needs N %% 128 == 0");
-  if (next_had_k != 0 && next_had_k != 16 && next_had_k != 32)
-    return fail(MRFP4_EUNSUPPORTED, "fused next-layer quantization: Hadamard block must be 0, 16 or 32");
+  if (next_had_k != 0 && next_had_k != 16 && next_had_k != 32 && next_had_k != 64 && next_had_k != 128)
+    return fail(MRFP4_EUNSUPPORTED, "fused next-layer quantization: Hadamard block must be 0, 16, 32, 64 or 128");
+  if (next_fmt == MRFP4_FMT_NVFP4 && !next_static_ts)
+    return fail(MRFP4_EUNSUPPORTED, "fused NVFP4 next-layer quantization needs a static global scale "
+                                    "(the whole-output max is not known inside the GEMM)");
   if (y_bf16 && (ldy < N || ldy % 16)) return fail(MRFP4_EINVAL, "bad output row stride");
   if (!a || !a_sf || !a_ts || !b || !b_sf || !b_ts || !next_codes || !next_sf || !next_tensor_scale || !status)
     return fail(MRFP4_EINVAL, "null buffer");
-  if (!aligned(next_codes, 16)) return fail(MRFP4_EUNSUPPORTED, "codes must be 16-byte aligned");
-  return cuda_status(mrfp4::launch_gemm_quant_next(a, a_sf, a_ts, b, b_sf, b_ts, y_bf16, ldy, M, N, K, fmt,
-                                                   next_had_k, next_codes, next_sf, next_tensor_scale, status,
-                                                   static_cast<cudaStream_t>(stream)),
-                     "mrfp4_gemm_quant_next");
+  if (!aligned(next_codes, 16) || !aligned(next_sf, 2)) return fail(MRFP4_EUNSUPPORTED, "codes must be 16-byte aligned");
+  return cuda_status(mrfp4::launch_gemm_quant_next(a, a_sf, a_ts, b, b_sf, b_ts, y_bf16, ldy, M, N, K, fmt, next_fmt,
+                                                   next_had_k, next_static_ts, next_codes, next_sf, next_tensor_scale,
+                                                   status, static_cast<cudaStream_t>(stream)),
+                     "mrfp4_gemm_quant_next_ex");
 }
 
 int mrfp4_pairwise_sums(const double* a, const int64_t* starts, const int64_t* lens, int64_t nseg, double* out,

@@ -87,9 +87,10 @@ struct GemmArgs {
   // would produce from the bf16 output (quantizers.py:247-255).  d (bf16 Y) may be null.
   uint8_t* q_codes;
   uint8_t* q_sf;
-  float* q_ts;        // the next layer's tensor scale: f32(4/3) (quantizers.py:191, :206-207)
+  float* q_ts;        // the next layer's tensor scale: f32(4/3) (quantizers.py:191, :206-207) or the NVFP4 s_T
+  const float* q_static_ts;  // NVFP4 next layer: the given (static) global scale s_T
   uint32_t* q_status;
-  uint32_t q_cb;      // scale column blocks of the next layer: N / 32 / 4
+  uint32_t q_cb;      // scale column blocks of the next layer: N / G / 4
   int64_t q_rows_pad; // ceil(M / 128) * 128
   qc::AQParams qp;    // c64 / kraw / kmx / pm of the next layer's rotation
   // Fused output all-gather (SURVEY.md 8(f) row f1, 2-CTA kernel, bf16): every output row
@@ -103,7 +104,9 @@ struct GemmArgs {
   uint32_t* sk_cnt;
 };
 constexpr size_t kSplitkHeader = 4096;   // counters, ahead of the fp32 partials in the workspace
-constexpr int kOutMxq = 100;  // internal OUT tag (not an ABI dtype)
+constexpr int kOutMxq = 100;  // internal OUT tags (not ABI dtypes): bf16 output quantized for the next
+constexpr int kOutNvq = 101;  // layer in MXFP4 / in NVFP4 with a static global scale
+__host__ __device__ constexpr bool is_quant_out(int out) { return out == kOutMxq || out == kOutNvq; }
 
 // Swizzled scale-factor offset (128 x 4 atoms), 32-bit.
 __device__ __forceinline__ uint32_t sf_off32q(uint32_t r, uint32_t c, uint32_t cb) {
@@ -574,38 +577,92 @@ __device__ __forceinline__ void issue_stage_tail(int nk, uint32_t el, uint32_t d
   }
 }
 
-// Next-layer MXFP4 quantization of one output row's 128 bf16 columns (4 groups of 32) --
-// the K1 arithmetic (quant_core.cuh) on the values K1 would read back from Y.  Padding rows
-// [M, rows_pad) get zero scale bytes, as K1 writes them.
-template <int HKQ>
-__device__ __forceinline__ void quant_next_row(const GemmArgs& g, int64_t row, int64_t col0, const uint32_t (&pkd)[64]) {
+// Next-layer quantization of one output row's 128 bf16 columns (4 segments of 32) -- the K1
+// arithmetic (quant_core.cuh) on the values K1 would read back from Y: MXFP4 (OUT == kOutMxq),
+// or NVFP4 against a given global scale (kOutNvq; the whole-Y max would need all of Y first).
+// Rotation: k <= 32 inside each segment; k = 64 / 128 span 2 / 4 segments of the row, so the
+// cross-segment butterfly stages (block element bits 5, 6) run in registers after the 32-point
+// transforms -- the FWHT stage order of K1.  Padding rows [M, rows_pad) get zero scale bytes.
+template <int OUT, int HKQ>
+__device__ __forceinline__ void quant_next_row(const GemmArgs& g, const qc::EncConsts& k, int64_t row, int64_t col0,
+                                               const uint32_t (&pkd)[64]) {
   using namespace qc;
+  constexpr bool kNv = OUT == kOutNvq;
+  constexpr int G = kNv ? 16 : 32;
   if (row >= g.M) {
     if (row < g.q_rows_pad)
 #pragma unroll
-      for (int c = 0; c < 4; ++c) g.q_sf[sf_off32q((uint32_t)row, (uint32_t)((col0 >> 5) + c), g.q_cb)] = 0;
+      for (int c = 0; c < 128 / G; ++c) g.q_sf[sf_off32q((uint32_t)row, (uint32_t)(col0 / G + c), g.q_cb)] = 0;
     return;
   }
   uint32_t bad = 0;
-#pragma unroll 1
-  for (int c = 0; c < 4; ++c) {
-    u64 P[kPairs];
+  auto encode = [&](const u64 (&P)[kPairs], int c) {
+    float a0, a1;
+    half_amax(P, a0, a1);
+    GroupScale s0, s1;
+    if constexpr (kNv) {
+      s0 = nv_group_scale(a0, g.qp, k.kenc, k.knv, k.st32, k.st64, k.zero_code);
+      s1 = nv_group_scale(a1, g.qp, k.kenc, k.knv, k.st32, k.st64, k.zero_code);
+      if (__float_as_uint(a0) >= 0x7f800000u || __float_as_uint(a1) >= 0x7f800000u) bad |= MRFP4_STATUS_NONFINITE;
+      if (s0.code == 0 || s1.code == 0) bad |= MRFP4_STATUS_SCALE_UNDERFLOW;
+    } else {
+      const float a = max3n(a0, a1, 0.f);
+      if (__float_as_uint(a) >= 0x7f800000u) bad |= MRFP4_STATUS_NONFINITE;
+      s0 = mx_group_scale(a, g.qp);
+      s1 = s0;
+    }
+    uint32_t w4[4];
+    quantize_seg(P, s0, s1, k.st32, g.qp, w4);
+    *reinterpret_cast<uint4*>(g.q_codes + row * (g.N >> 1) + ((col0 + 32 * c) >> 1)) =
+        make_uint4(w4[0], w4[1], w4[2], w4[3]);
+    if constexpr (kNv)   // columns 2c, 2c+1 of the 16-element groups share a 16-bit word of the layout
+      *reinterpret_cast<uint16_t*>(g.q_sf + sf_off32q((uint32_t)row, (uint32_t)(col0 / 16 + 2 * c), g.q_cb)) =
+          (uint16_t)(s0.code | (s1.code << 8));
+    else
+      g.q_sf[sf_off32q((uint32_t)row, (uint32_t)(col0 / 32 + c), g.q_cb)] = (uint8_t)s0.code;
+  };
+  auto unpack = [&](u64 (&P)[kPairs], int c) {
 #pragma unroll
     for (int j = 0; j < kPairs; ++j) {
       const uint32_t w = pkd[16 * c + j];
       P[j] = pk(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
     }
-    if constexpr (HKQ > 0) fwht<HKQ>(P, 0, g.qp.pm);
-    float a0, a1;
-    half_amax(P, a0, a1);
-    const float a = max3n(a0, a1, 0.f);
-    if (__float_as_uint(a) >= 0x7f800000u) bad |= MRFP4_STATUS_NONFINITE;
-    const GroupScale s0 = mx_group_scale(a, g.qp);
-    uint32_t w4[4];
-    quantize_seg(P, s0, s0, 1.33333337306976318359375f, g.qp, w4);
-    *reinterpret_cast<uint4*>(g.q_codes + row * (g.N >> 1) + ((col0 + 32 * c) >> 1)) =
-        make_uint4(w4[0], w4[1], w4[2], w4[3]);
-    g.q_sf[sf_off32q((uint32_t)row, (uint32_t)((col0 >> 5) + c), g.q_cb)] = (uint8_t)s0.code;
+  };
+  if constexpr (HKQ <= 32) {
+#pragma unroll 1
+    for (int c = 0; c < 4; ++c) {
+      u64 P[kPairs];
+      unpack(P, c);
+      if constexpr (HKQ > 0) fwht<HKQ>(P, 0, g.qp.pm);
+      encode(P, c);
+    }
+  } else {
+    u64 P[4][kPairs];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      unpack(P[c], c);
+      fwht<32>(P[c], 0, g.qp.pm);
+    }
+#pragma unroll
+    for (int c = 0; c < 4; c += 2)          // bit 5: segments (c, c + 1)
+#pragma unroll
+      for (int j = 0; j < kPairs; ++j) {
+        const u64 a = P[c][j], b = P[c + 1][j];
+        P[c][j] = add2(a, b);
+        P[c + 1][j] = sub2(a, b);
+      }
+    if constexpr (HKQ >= 128) {
+#pragma unroll
+      for (int c = 0; c < 2; ++c)           // bit 6: segments (c, c + 2)
+#pragma unroll
+        for (int j = 0; j < kPairs; ++j) {
+          const u64 a = P[c][j], b = P[c + 2][j];
+          P[c][j] = add2(a, b);
+          P[c + 2][j] = sub2(a, b);
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) encode(P[c], c);
   }
   if (bad) atomic_or_status(g.q_status, bad);
 }
@@ -845,8 +902,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<VEC>::kThreads2
     const int q = warp & 3, h = (warp - C::kEpiWarp0) >> 2;
     pdl_wait();
     const float alpha = __ldg(g.a_ts) * __ldg(g.b_ts);
-    if constexpr (OUT == kOutMxq)
-      if (blockIdx.x == 0 && warp == 6 && lane == 0) *g.q_ts = 1.33333337306976318359375f;
+    qc::EncConsts qk;   // the next layer's encode constants (MXFP4: ts = f32(4/3))
+    if constexpr (OUT == kOutNvq) qk = qc::nv_consts_st(g.qp, __ldg(g.q_static_ts));
+    if constexpr (is_quant_out(OUT))
+      if (blockIdx.x == 0 && warp == C::kEpiWarp0 && lane == 0) *g.q_ts = qk.st32;
     uint32_t acc_phase = 0;
     auto release_acc = [&] {
       sm100::tc_fence_before();
@@ -866,7 +925,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<VEC>::kThreads2
       const int64_t row = (int64_t)m_blk * 256 + rank * 128 + q * 32 + lane;
       const int64_t col0 = (int64_t)n_blk * 256 + h * 128;
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + h * 128;
-      if constexpr (OUT == MRFP4_DT_BF16 || OUT == kOutMxq) {
+      if constexpr (OUT == MRFP4_DT_BF16 || is_quant_out(OUT)) {
         uint32_t pkd[64];
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
@@ -880,8 +939,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<VEC>::kThreads2
           }
         }
         release_acc();
-        if constexpr (OUT == kOutMxq) {
-          if (col0 < g.N) quant_next_row<HKQ>(g, row, col0, pkd);
+        if constexpr (is_quant_out(OUT)) {
+          if (col0 < g.N) quant_next_row<OUT, HKQ>(g, qk, row, col0, pkd);
           if (!g.d) continue;
         }
         if (row < g.M) {
@@ -1158,11 +1217,12 @@ int launch_gemm_peers(const uint8_t* a, const uint8_t* a_sf, const float* a_ts, 
   return fmt == MRFP4_FMT_NVFP4 ? launch2<16, MRFP4_DT_BF16>(a, b, g, s) : launch2<32, MRFP4_DT_BF16>(a, b, g, s);
 }
 
-// K2 with the next layer's MXFP4 act-quant fused into the epilogue (2-CTA kernel only).
+// K2 with the next layer's act-quant fused into the epilogue (2-CTA kernel only): MXFP4, or
+// NVFP4 against a given global scale (next_static_ts).
 int launch_gemm_quant_next(const uint8_t* a, const uint8_t* a_sf, const float* a_ts, const uint8_t* b,
                            const uint8_t* b_sf, const float* b_ts, void* y, int64_t ldy, int64_t M, int64_t N,
-                           int64_t K, int fmt, int next_hk, uint8_t* q_codes, uint8_t* q_sf, float* q_ts,
-                           uint32_t* q_status, cudaStream_t s) {
+                           int64_t K, int fmt, int next_fmt, int next_hk, const float* next_static_ts,
+                           uint8_t* q_codes, uint8_t* q_sf, float* q_ts, uint32_t* q_status, cudaStream_t s) {
   GemmArgs g{};
   g.b = b;
   g.preissue = g_preissue;
@@ -1179,7 +1239,8 @@ int launch_gemm_quant_next(const uint8_t* a, const uint8_t* a_sf, const float* a
   g.q_sf = q_sf;
   g.q_ts = q_ts;
   g.q_status = q_status;
-  g.q_cb = (uint32_t)(N / 128);
+  g.q_static_ts = next_static_ts;
+  g.q_cb = (uint32_t)(N / (next_fmt == MRFP4_FMT_NVFP4 ? 64 : 128));
   g.q_rows_pad = ceil_div(M, 128) * 128;
   const double c64 = next_hk ? 1.0 / std::sqrt((double)next_hk) : 1.0;
   g.qp.c64 = c64;
@@ -1187,15 +1248,23 @@ int launch_gemm_quant_next(const uint8_t* a, const uint8_t* a_sf, const float* a
   g.qp.kmx = (float)(c64 / (double)1.33333337306976318359375f);
   const float pm[2] = {1.f, -1.f};
   memcpy(&g.qp.pm, pm, sizeof(pm));
-  auto go = [&](auto vec_tag) {
-    constexpr int V = decltype(vec_tag)::value;
+  auto go = [&](auto vec_tag, auto out_tag) {
+    constexpr int V = decltype(vec_tag)::value, O = decltype(out_tag)::value;
     switch (next_hk) {
-      case 16: return launch2<V, kOutMxq, 16>(a, b, g, s);
-      case 32: return launch2<V, kOutMxq, 32>(a, b, g, s);
-      default: return launch2<V, kOutMxq, 0>(a, b, g, s);
+      case 16: return launch2<V, O, 16>(a, b, g, s);
+      case 32: return launch2<V, O, 32>(a, b, g, s);
+      case 64: return launch2<V, O, 64>(a, b, g, s);
+      case 128: return launch2<V, O, 128>(a, b, g, s);
+      default: return launch2<V, O, 0>(a, b, g, s);
     }
   };
-  return fmt == MRFP4_FMT_NVFP4 ? go(std::integral_constant<int, 16>{}) : go(std::integral_constant<int, 32>{});
+  using I16 = std::integral_constant<int, 16>;
+  using I32 = std::integral_constant<int, 32>;
+  using Mx = std::integral_constant<int, kOutMxq>;
+  using Nv = std::integral_constant<int, kOutNvq>;
+  if (next_fmt == MRFP4_FMT_NVFP4)
+    return fmt == MRFP4_FMT_NVFP4 ? go(I16{}, Nv{}) : go(I32{}, Nv{});
+  return fmt == MRFP4_FMT_NVFP4 ? go(I16{}, Mx{}) : go(I32{}, Mx{});
 }
 
 }  // namespace mrfp4

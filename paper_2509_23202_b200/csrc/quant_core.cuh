@@ -276,6 +276,25 @@ __device__ __forceinline__ GroupScale nv_group_scale(float amax, const AQParams&
   return g;
 }
 
+// Per-launch encode constants.  MXFP4: ts = f32(4/3) (quantizers.py:34,191).  NVFP4: derived
+// from the whole-tensor max exactly as numpy does (quantizers.py:187, :198-200).
+struct EncConsts {
+  float st32 = 1.33333337306976318359375f;
+  double st64 = 1.0;
+  float kenc = 0.f, knv = 0.f;
+  uint32_t zero_code = 0;
+};
+
+__device__ __forceinline__ EncConsts nv_consts_st(const AQParams& p, float st32) {
+  EncConsts k;
+  k.st32 = st32;
+  k.st64 = (double)k.st32;
+  k.zero_code = e4m3_rne64(1.0 / k.st64);                               // raw = 1.0 sentinel
+  k.kenc = __double2float_rn(p.c64 / 6.0 / k.st64);
+  k.knv = __double2float_rn(p.c64 / k.st64);
+  return k;
+}
+
 // Codes of the segment as 4 words (word w = elements 8w..8w+7 = pairs 4w..4w+3).
 // s0 scales pairs 0..7 (elements 0..15), s1 pairs 8..15.
 __device__ __forceinline__ void quantize_seg(const u64 (&P)[kPairs], const GroupScale& s0, const GroupScale& s1,

@@ -311,16 +311,29 @@ def quantized_linear_host(x: torch.Tensor, w: PackedWeight, *, out: torch.Tensor
     return out
 
 
-def quantized_linear_requant(x, w: PackedWeight, next_transform=None, *, keep_output: bool = False,
-                             check: bool = False):
+def quantized_linear_requant(x, w: PackedWeight, next_transform=None, *, next_spec=None, next_tensor_scale=None,
+                             keep_output: bool = False, check: bool = False):
     """``quantized_linear`` whose bf16 output is quantized for the NEXT layer in K2's epilogue
     (SURVEY.md 8(f) row f4): returns the GpuQuantResult that
-    ``quantize_rtn(y, FormatSpec.mxfp4(), transform=next_transform)`` would return for
+    ``quantize_rtn(y, next_spec, transform=next_transform)`` would return for
     y = quantized_linear(x, w) -- bit-identical -- without writing y to HBM and reading it back
-    (``keep_output=True`` also returns y).  MXFP4 only (NVFP4's tensor scale is a max over all
-    of y); next_transform: None or a Hadamard block of 16 / 32."""
+    (``keep_output=True`` also returns y).
+    next_spec: FormatSpec.mxfp4() (default), or FormatSpec.nvfp4() with ``next_tensor_scale`` --
+    a static global scale s_T (float or device float32 tensor), i.e.
+    ``quantize_rtn(y, nvfp4, transform, static_tensor_scale=s_T)``: a whole-y s_T (quantizers.py:
+    195-200) needs all of y before any group is encoded, so it cannot be fused.
+    next_transform: None or a Hadamard block of 16 / 32 / 64 / 128."""
     if not isinstance(w, PackedWeight):
         w = prepare_weight(w)
+    nfmt = FMT_MXFP4_CODE if next_spec is None else format_code(next_spec)
+    st = None
+    if nfmt == FMT_NVFP4_CODE:
+        if next_tensor_scale is None:
+            raise DataError("unsupported on GPU path: a fused NVFP4 requant needs a static next_tensor_scale")
+        from .quantize import _static_ts
+        st = _static_ts(next_tensor_scale, nfmt, w.device)
+    elif next_tensor_scale is not None:
+        raise DataError("next_tensor_scale applies to an NVFP4 next layer only")
     x2 = as_device_matrix(x, w.device)
     M, K = x2.shape
     if K != w.K:
@@ -328,15 +341,16 @@ def quantized_linear_requant(x, w: PackedWeight, next_transform=None, *, keep_ou
     hk = hadamard_block(next_transform)
     a = alloc_result(M, K, w.fmt, w.had_k, x2.device)
     act_quant_into(x2, w.fmt, w.had_k, a.codes, a.sf, a.tensor_scale_dev, a.scratch)
-    res = alloc_result(M, w.N, FMT_MXFP4_CODE, hk, x2.device)
+    res = alloc_result(M, w.N, nfmt, hk, x2.device)
     y = torch.empty((M, w.N), dtype=torch.bfloat16, device=x2.device) if keep_output else None
     L = _lib.lib()
-    _lib.check(L.mrfp4_gemm_quant_next(
-        _lib.ptr(a.codes), _lib.ptr(a.sf), _lib.ptr(a.tensor_scale_dev),
-        _lib.ptr(w.codes), _lib.ptr(w.sf), _lib.ptr(w.tensor_scale_dev),
-        _lib.ptr(y) if y is not None else None, w.N, M, w.N, K, w.fmt, hk,
-        _lib.ptr(res.codes), _lib.ptr(res.sf), _lib.ptr(res.tensor_scale_dev), _lib.ptr(res.scratch),
-        _lib.stream_ptr(torch, x2.device)))
+    with torch.cuda.device(x2.device):
+        _lib.check(L.mrfp4_gemm_quant_next_ex(
+            _lib.ptr(a.codes), _lib.ptr(a.sf), _lib.ptr(a.tensor_scale_dev),
+            _lib.ptr(w.codes), _lib.ptr(w.sf), _lib.ptr(w.tensor_scale_dev),
+            _lib.ptr(y) if y is not None else None, w.N, M, w.N, K, w.fmt, nfmt, hk, _lib.ptr(st),
+            _lib.ptr(res.codes), _lib.ptr(res.sf), _lib.ptr(res.tensor_scale_dev), _lib.ptr(res.scratch),
+            _lib.stream_ptr(torch, x2.device)))
     if check:
         res.check()
     return (res, y) if keep_output else res

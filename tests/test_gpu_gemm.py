@@ -240,8 +240,39 @@ def test_requant_rejects_unsupported():
     with pytest.raises(P.DataError):
         P.quantized_linear_requant(X, w)
     X2 = torch.from_numpy(O.bf16_round(rng.standard_normal((256, 512)))).cuda().bfloat16()
+    with pytest.raises(P.DataError, match="static"):   # whole-y NVFP4 s_T cannot be fused
+        P.quantized_linear_requant(X2, w, next_spec=SPEC["nvfp4"])
     with pytest.raises(P.DataError):
-        P.quantized_linear_requant(X2, w, P.TransformSpec.hadamard(128))
+        P.quantized_linear_requant(X2, w, next_tensor_scale=1.0)   # MXFP4 has no global scale
+
+
+@pytest.mark.parametrize("next_fmt,next_k", [("mxfp4", 64), ("mxfp4", 128), ("nvfp4", 0), ("nvfp4", 16),
+                                             ("nvfp4", 64), ("nvfp4", 128)])
+@pytest.mark.parametrize("M,N,K", [(256, 1024, 2048), (300, 2048, 1024)])
+def test_requant_epilogue_all_blocks_and_nvfp4_static(next_fmt, next_k, M, N, K):
+    """Next-layer requant with H64 / H128 (cross-segment stages inside the epilogue thread) and
+    NVFP4 against a static global scale: byte-identical to K1 on the bf16 output, and to the
+    oracle (quantize_rtn with that s_global) at the north-star bar."""
+    rng = np.random.default_rng(M + N + next_k)
+    X = torch.from_numpy(O.bf16_round(rng.standard_normal((M, K)))).cuda().bfloat16()
+    W = torch.from_numpy(O.bf16_round(rng.standard_normal((N, K)) / np.sqrt(K))).cuda().bfloat16()
+    w = P.quantize_weight(W, SPEC["mxfp4"], P.TransformSpec.hadamard(32))
+    tr = P.TransformSpec.hadamard(next_k) if next_k else None
+    y_ref = P.quantized_linear(X, w)
+    st = None
+    if next_fmt == "nvfp4":   # e.g. calibrated offline: 0.8 x this batch's dynamic s_T (some groups saturate)
+        st = float(np.float32(P.quantize_rtn(y_ref, SPEC["nvfp4"], transform=tr).tensor_scale * 0.8))
+    q, y = P.quantized_linear_requant(X, w, tr, next_spec=SPEC[next_fmt], next_tensor_scale=st, keep_output=True,
+                                      check=True)
+    assert torch.equal(y, y_ref)
+    ref = P.quantize_rtn(y_ref, SPEC[next_fmt], transform=tr, static_tensor_scale=st)
+    assert torch.equal(q.codes, ref.codes) and torch.equal(q.sf, ref.sf)
+    assert q.tensor_scale == ref.tensor_scale
+    ora = O.quantize_rtn(y_ref.float().cpu().numpy().astype(np.float64), next_fmt, hadamard=next_k or None,
+                         static_ts=st)
+    ec = O.unpack_nibbles(q.codes.cpu().numpy(), M * N).reshape(M, N)
+    assert (ec == ora.element_codes).mean() >= 0.9999
+    assert (q.scale_codes().cpu().numpy() == ora.scale_codes).mean() >= 0.9999
 
 
 @pytest.mark.parametrize("fmt,k,M", [("nvfp4", 16, 16), ("mxfp4", 32, 16), ("nvfp4", 128, 256), ("mxfp4", 32, 512)])
