@@ -316,7 +316,7 @@ def quantize(X, spec, policy=None, transform=None, *, check: bool = True) -> Gpu
     """``microfp.quantize`` dispatch (quantizers.py:341-347): ScaleMode.MSE runs the MSE scale
     search (``mse_optimize_scales``) on the GPU, anything else is ``quantize_rtn``."""
     if _is_mse(policy):
-        return mse_optimize_scales(X, spec, transform=transform, policy=policy)
+        return mse_optimize_scales(X, spec, transform=transform, policy=policy, check=check)
     return quantize_rtn(X, spec, policy=policy, transform=transform, check=check)
 
 
@@ -401,7 +401,7 @@ class _NpSum:
         return ev(self.tree)
 
 
-def mse_optimize_scales(X, spec, transform=None, policy=None) -> GpuQuantResult:
+def mse_optimize_scales(X, spec, transform=None, policy=None, *, check: bool = True) -> GpuQuantResult:
     """``quantize_rtn`` with MSE-optimised scales on the GPU (quantizers.py:330-337,
     ``optimize_group_scales`` :263-327).
 
@@ -412,7 +412,14 @@ def mse_optimize_scales(X, spec, transform=None, policy=None) -> GpuQuantResult:
     are computed by ``mrfp4_mse_pass`` / ``mrfp4_mse_group_err`` in float64 with numpy's
     summation order, and their totals are summed with numpy, so the decisions are the
     reference's.  Raises ``DataError`` where the reference does (non-finite input; a candidate
-    scale that decodes to 0)."""
+    scale that decodes to 0).
+
+    MXFP4 (no tensor-scale scan) is "online": every round's pass repeats the first with the same
+    s_global, so the reference's loop always stops after one repeat; one pass decides, with no
+    host round trip -- rotate + absmax + one mrfp4_mse_pass on the stream (QuTLASS's fused MSE
+    activation quantizer).  ``check=False`` then leaves the DataError conditions
+    in the status word (``.check()``).  NVFP4's s_T scan needs the candidates' whole-tensor
+    totals, which are summed in numpy's order on the host (offline weights)."""
     fmt = format_code(spec)
     _check_policy(policy, fmt, mse=True)
     had_k = hadamard_block(transform)
@@ -423,7 +430,8 @@ def mse_optimize_scales(X, spec, transform=None, policy=None) -> GpuQuantResult:
         raise DataError(f"columns ({K}) not divisible by group size ({G})")
     if had_k and K % had_k:
         raise DataError(f"columns ({K}) not divisible by transform block ({had_k})")
-    if not bool(torch.isfinite(X).all()):                                  # quantizers.py:99-100
+    is_global = fmt == FMT_NVFP4
+    if is_global and not bool(torch.isfinite(X).all()):                    # quantizers.py:99-100
         raise DataError("non-finite element")
     dev = X.device
     L = _lib.lib()
@@ -433,7 +441,6 @@ def mse_optimize_scales(X, spec, transform=None, policy=None) -> GpuQuantResult:
     B = Y.view(ng, G)
     absmax = B.abs().amax(dim=1)
     raw0 = torch.where(absmax == 0, torch.ones_like(absmax), absmax / 6.0).contiguous()
-    is_global = fmt == FMT_NVFP4
     s_global, factor = 1.0, 1.0
     if is_global:                                                         # quantizers.py:195-200
         top = float(absmax.max()) / 6.0
@@ -467,6 +474,22 @@ def mse_optimize_scales(X, spec, transform=None, policy=None) -> GpuQuantResult:
         _lib.check(L.mrfp4_mse_group_err(_lib.ptr(Y), ng, fmt, _lib.ptr(dec), ts, _lib.ptr(gerr2), status, stream))
         return whole_sum.total(gerr2)
 
+    if not is_global:   # MXFP4: one pass decides (see above); no totals, no host round trip
+        ts = float(np.float32(s_global * factor))
+        _lib.check(L.mrfp4_mse_pass(_lib.ptr(Y), ng, fmt, _lib.ptr(cand), len(cand_np), _lib.ptr(raw0), s_global, ts,
+                                    _lib.ptr(sc), _lib.ptr(dec), _lib.ptr(gerr), _lib.ptr(codes), status, stream))
+        res = alloc_result(M, K, fmt, had_k, dev, scratch)
+        res.codes = codes
+        _lib.check(L.mrfp4_sf_swizzle(_lib.ptr(sc), _lib.ptr(res.sf), M, K // G, stream))
+        res.tensor_scale_dev.fill_(ts)
+        res.source = X
+        if check:
+            st = res.status
+            if st & _lib.STATUS_SCALE_UNDERFLOW:
+                raise DataError("non-finite element (a candidate group scale underflows the scale format)")
+            if st & _lib.STATUS_NONFINITE:
+                raise DataError("non-finite element")
+        return res
     best_total = pass_groups(s_global)
     for _ in range(MSE_SEARCH_ROUNDS):
         if is_global:
