@@ -227,6 +227,19 @@ int mrfp4_mse_pass(const double* y, int64_t ngroups, int fmt, const double* cand
                    uint8_t* codes, uint32_t* status, void* stream);
 int mrfp4_mse_group_err(const double* y, int64_t ngroups, int fmt, const double* decoded, double ts,
                         double* group_err, uint32_t* status, void* stream);
+/*
+ * GPTQ column solver, one lazy block (replaces the inner loop of
+ * _gptq_core, gptq.py:148-167): for columns i1 .. i1+block-1 (block <= 128) of the permuted
+ * weight W [rows, d] (float64, row-major, updated in place), column scales S [rows, d] and the
+ * upper inverse-Cholesky factor T [d, d]: per column, codes / q = fp4_round_codes(w / s) (E2M1
+ * code per element, written unpacked to codes [rows, d]; q to Q [rows, d]), e = (w - q) / T[i, i]
+ * to err [rows, 128] (column i - i1), and w_j -= e * T[i, j] for the block's later columns -- the
+ * reference's float64 operations, unfused.  The caller applies W[:, i1+block:] -= err @ T[block
+ * rows, i1+block:] (gptq.py:165-166).
+ */
+int mrfp4_gptq_block(double* W, const double* S, const double* T, int64_t rows, int64_t d, int i1, int block,
+                     double* Q, uint8_t* codes, double* err, void* stream);
+
 /* out[i] = numpy's pairwise sum (np.sum) of a[starts[i] .. starts[i] + lens[i]) -- the segment
  * sums the MSE driver combines on the host in numpy's order (bit-identical totals). */
 int mrfp4_pairwise_sums(const double* a, const int64_t* starts, const int64_t* lens, int64_t nseg, double* out,

@@ -12,6 +12,7 @@ for everything on the path ``Q(X H_k) Q(W H_k)^T``:
     quantized_linear_host            the same on host buffers, H2D / compute / D2H pipelined
     quantized_linear_requant         K2 + the next layer's MXFP4 act-quant fused in its epilogue
     GraphedLinear                    a fixed-shape quantized_linear captured into a CUDA graph
+    gptq.gptq_quantize / mr_gptq     GPU GPTQ / MR-GPTQ solver (offline weights)
     quantized_linear_sharded         N-sharded linear + NCCL all-gather
 
 All compute runs in libmrfp4.so (sm_100a); there is no CPU fallback.
@@ -36,6 +37,9 @@ __all__ = [
     "quantized_linear_sharded", "read_quant", "write_quant", "parse_quant", "quant_bytes",
     "FMT_MXFP4", "FMT_NVFP4",
 ]
+
+
+from . import gptq  # noqa: E402
 
 
 def __getattr__(name):

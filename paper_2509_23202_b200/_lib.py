@@ -56,6 +56,7 @@ SIGNATURES = {
     "mrfp4_mse_group_err": (_int, [_vp, _i64, _int, _vp, _c.c_double, _vp, _vp, _vp]),
     "mrfp4_gemm_peers": (_int, [_vp, _vp, _vp, _vp, _vp, _vp, _c.POINTER(_vp), _int, _i64, _i64, _i64, _i64, _int,
                                 _vp]),
+    "mrfp4_gptq_block": (_int, [_vp, _vp, _vp, _i64, _i64, _int, _int, _vp, _vp, _vp, _vp]),
     "mrfp4_pairwise_sums": (_int, [_vp, _vp, _vp, _i64, _vp, _vp]),
 }
 

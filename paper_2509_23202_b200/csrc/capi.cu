@@ -13,6 +13,8 @@ namespace mrfp4 {
 int launch_act_quant(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ldx, int fmt, int hk, uint8_t* codes,
                      uint8_t* sf, float* tensor_scale, uint32_t* status, void* workspace,
                      const mrfp4_act_quant_opts* opts, cudaStream_t s);
+int launch_gptq_block(double* W, const double* S, const double* T, int64_t rows, int64_t d, int i1, int B, double* Q,
+                      uint8_t* codes, double* Err, cudaStream_t s);
 int launch_rotate_f64(const double* x, int64_t M, int64_t K, int64_t ldx, int hk, double* y, cudaStream_t s);
 int launch_gemm_fp4(const uint8_t* a, const uint8_t* a_sf, const float* a_ts, const uint8_t* b, const uint8_t* b_sf,
                     const float* b_ts, void* d, int d_dtype, int64_t M, int64_t N, int64_t K, int64_t ldd, int fmt,
@@ -140,6 +142,17 @@ int mrfp4_rotate_f64(const double* x, int64_t M, int64_t K, int64_t ldx, int had
   if (ldx < K || !x || !y) return fail(MRFP4_EINVAL, "bad arguments");
   return cuda_status(mrfp4::launch_rotate_f64(x, M, K, ldx, had_k, y, static_cast<cudaStream_t>(stream)),
                      "mrfp4_rotate_f64");
+}
+
+int mrfp4_gptq_block(double* W, const double* S, const double* T, int64_t rows, int64_t d, int i1, int block,
+                     double* Q, uint8_t* codes, double* err, void* stream) {
+  if (rows < 1 || d < 1 || i1 < 0 || block < 1 || block > 128 || i1 + block > d)
+    return fail(MRFP4_EINVAL, "bad GPTQ block (rows %lld, d %lld, i1 %d, block %d; block <= 128)", (long long)rows,
+                (long long)d, i1, block);
+  if (!W || !S || !T || !Q || !codes || !err) return fail(MRFP4_EINVAL, "null buffer");
+  return cuda_status(mrfp4::launch_gptq_block(W, S, T, rows, d, i1, block, Q, codes, err,
+                                              static_cast<cudaStream_t>(stream)),
+                     "mrfp4_gptq_block");
 }
 
 int mrfp4_quant_metrics(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ldx, int fmt, int had_k,

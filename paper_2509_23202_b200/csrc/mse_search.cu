@@ -248,3 +248,77 @@ int launch_np_pairwise_segments(const double* a, const int64_t* starts, const in
 }
 
 }  // namespace mrfp4
+
+// ---------------------------------------------------------------------------
+// GPTQ column solver: one lazy block of _gptq_core
+// (/root/reference/pkg/src/microfp/gptq.py:148-167) for all rows at once.  Rows are
+// independent given T and the column scales, so a thread owns one row: the block's columns
+// i1 .. i1+B-1 of its row sit in shared memory ([B][threads], conflict-free), the block of the
+// upper factor T ([B][B]) is shared by the CTA.  Per column i, in the reference's float64
+// arithmetic (no FMA contraction):
+//     codes, vals = fp4_round_codes(w_i / s_i); q = s_i * vals          (:141-145)
+//     e = (w_i - q) / T[i, i];  w_j -= e * T[i, j]  for i < j < B          (:160-164)
+// The caller applies the lazy trailing update W[:, i2:] -= Err @ T[i1:i2, i2:] (:165-166) as a
+// float64 GEMM.
+// ---------------------------------------------------------------------------
+namespace mrfp4 {
+namespace {
+
+constexpr int kGptqThreads = 64;
+constexpr int kGptqMaxB = 128;
+
+__global__ void __launch_bounds__(kGptqThreads, 1)
+    k_gptq_block(double* __restrict__ W, const double* __restrict__ S, const double* __restrict__ T, int64_t rows,
+                 int64_t d, int i1, int B, double* __restrict__ Q, uint8_t* __restrict__ codes,
+                 double* __restrict__ Err) {
+  extern __shared__ __align__(16) double gsm[];
+  double* Tb = gsm;                          // [B][B] block of T (row i, column j)
+  double* Wb = gsm + kGptqMaxB * kGptqMaxB;  // [B][kGptqThreads]
+  const int tid = threadIdx.x;
+  for (int x = tid; x < B * B; x += blockDim.x) {
+    const int i = x / B, j = x - i * B;
+    Tb[i * B + j] = T[(int64_t)(i1 + i) * d + i1 + j];
+  }
+  const int64_t r = (int64_t)blockIdx.x * kGptqThreads + tid;
+  const bool live = r < rows;
+  if (live)
+    for (int j = 0; j < B; ++j) Wb[j * kGptqThreads + tid] = W[r * d + i1 + j];
+  __syncthreads();
+  if (!live) return;
+  const double* Sr = S + r * d + i1;
+  for (int i = 0; i < B; ++i) {
+    const double wi = Wb[i * kGptqThreads + tid];
+    const double si = Sr[i];
+    uint32_t c;
+    const double q = __dmul_rn(si, fp4_round64(__ddiv_rn(wi, si), c));
+    const double e = __ddiv_rn(__dsub_rn(wi, q), Tb[i * B + i]);
+    Q[r * d + i1 + i] = q;
+    codes[r * d + i1 + i] = (uint8_t)c;
+    Err[r * kGptqMaxB + i] = e;
+    const double* Ti = Tb + i * B;
+#pragma unroll 4
+    for (int j = i + 1; j < B; ++j) {
+      double* wj = Wb + j * kGptqThreads + tid;
+      *wj = __dsub_rn(*wj, __dmul_rn(e, Ti[j]));
+    }
+  }
+}
+
+}  // namespace
+
+int launch_gptq_block(double* W, const double* S, const double* T, int64_t rows, int64_t d, int i1, int B, double* Q,
+                      uint8_t* codes, double* Err, cudaStream_t s) {
+  if (B < 1 || B > kGptqMaxB) return MRFP4_EINVAL;
+  const size_t smem = (size_t)(kGptqMaxB * kGptqMaxB + kGptqMaxB * kGptqThreads) * sizeof(double);
+  static std::atomic<int> attr[kMaxDevices];
+  if (per_device_once(attr, [&] {
+        return cudaFuncSetAttribute(k_gptq_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) ==
+                       cudaSuccess ? 1 : -1;
+      }) < 0)
+    return MRFP4_ECUDA;
+  const int grid = (int)ceil_div(rows, kGptqThreads);
+  k_gptq_block<<<grid, kGptqThreads, smem, s>>>(W, S, T, rows, d, i1, B, Q, codes, Err);
+  return cudaPeekAtLastError() == cudaSuccess ? MRFP4_OK : MRFP4_ECUDA;
+}
+
+}  // namespace mrfp4

@@ -81,6 +81,9 @@ def prepare_weight(w, device=None) -> PackedWeight:
     if isinstance(w, PackedWeight):
         return w
     if isinstance(w, GpuQuantResult):
+        if getattr(w, "scale_fit", None) is not None:
+            raise DataError("unsupported on GPU path: scale_fit weights (fitted E8M0 grid 2^(a*q+b) is not "
+                            "hardware E8M0; quantize with absmax scales)")
         _validate_gemm_k(w.cols)
         # The clone is a plain stream-ordered copy, i.e. an ordering point outside the PDL chain:
         # the GEMM issues its weight loads before griddepcontrol.wait, so it must never become a
