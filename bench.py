@@ -164,6 +164,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--M", type=int, default=0, help="override the config's token count (sweeps)")
+    ap.add_argument("--gather", default="auto", choices=["auto", "nccl", "fused"],
+                    help="N-sharded output gather: NCCL all-gather, the K2 epilogue's peer stores into "
+                         "symmetric memory, or (auto, N > 1) both, reporting the faster")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = CONFIGS[args.config]
@@ -184,11 +187,12 @@ def main():
 
     import paper_2509_23202_b200 as P
     from paper_2509_23202_b200.quantize import act_quant_into, alloc_result
-    from paper_2509_23202_b200.sharded import gather_columns
+    from paper_2509_23202_b200.sharded import PeerOutputs, gather_columns, gemm_into_peers
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    sharded = world > 1 or args.gather != "auto"
+    if sharded:
         dist.init_process_group("nccl", device_id=dev)
 
     name, M, K, N, fmt, had = cfg
@@ -200,7 +204,7 @@ def main():
     g.manual_seed(4321)
     w_dense = (torch.randn((N, K), generator=g, device=dev, dtype=torch.float32) / K ** 0.5).bfloat16()
     w_full = P.quantize_weight(w_dense, spec, tr)            # GPU RTN == reference quantize_rtn(W, ..., H)
-    w = w_full.shard(rank, world) if world > 1 else w_full
+    w = w_full.shard(rank, world) if sharded else w_full
     a = alloc_result(M, K, w.fmt, had, dev)
     y = torch.empty((M, w.N), dtype=torch.bfloat16, device=dev)
     flush_w = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device=dev)
@@ -214,14 +218,35 @@ def main():
     # K1 (one launch for both formats) + K2 (split-K for small M reduces inside K2)
     launches_per_step = 2
 
-    def step():
+    # N-sharded: time-to-gathered-output, through the NCCL all-gather or the fused peer-store gather
+    gathers = []
+    if sharded:
+        gathers = ["nccl", "fused"] if args.gather == "auto" else [args.gather]
+    po = None
+    if "fused" in gathers:
+        try:
+            po = PeerOutputs(M, N, device=dev)
+        except Exception as e:  # symmetric memory unavailable: NCCL only
+            print(f"fused gather unavailable: {e!r}", file=sys.stderr)
+            gathers = [gg for gg in gathers if gg != "fused"] or ["nccl"]
+    cols = slice(rank * w.N, (rank + 1) * w.N)
+
+    def step_nccl():
         act_quant_into(x, w.fmt, had, a.codes, a.sf, a.tensor_scale_dev, a.scratch)
         P.gemm(a, w, y)
-        if world > 1:
-            gather_columns(y, None)  # time-to-gathered-output includes the NCCL all-gather
+        if sharded:
+            gather_columns(y, None)
+
+    def step_fused():
+        act_quant_into(x, w.fmt, had, a.codes, a.sf, a.tensor_scale_dev, a.scratch)
+        po.barrier(0)
+        gemm_into_peers(a, w, [pp[:, cols] for pp in po.peers])
+        po.barrier(1)
+
+    step = step_nccl
 
     def barrier():
-        if world > 1:
+        if sharded:
             dist.barrier()
         torch.cuda.synchronize(dev)
 
@@ -236,9 +261,13 @@ def main():
             e1.record(stream)
         return ev
 
-    for _ in range(args.warmup):
-        flush_l2()
-        step()
+    variants = {gg: (step_fused if gg == "fused" else step_nccl) for gg in gathers} or {"none": step_nccl}
+    for fn in variants.values():
+        for _ in range(args.warmup):
+            flush_l2()
+            fn()
+        barrier()
+
     def busy():   # local work only (no collective: ranks may loop a different number of times)
         for _ in range(10):
             flush_l2()
@@ -248,12 +277,21 @@ def main():
 
     # sampling runs from just before the timed region (under the same load) to its end
     sampler = ClockSampler(torch.cuda.current_device()).start(keep_busy=busy)
-    barrier()
-    ev_step = timed(step, args.steps)              # the timed region: exactly K steps
-    barrier()
+    t_var = {}
+    for gname, fn in variants.items():
+        barrier()
+        ev_step = timed(fn, args.steps)              # the timed region: exactly K steps
+        barrier()
+        t_v = sum(a_.elapsed_time(b_) * 1e-3 for a_, b_ in ev_step) / args.steps
+        if sharded:                                  # max over ranks
+            tt = torch.tensor([t_v], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t_v = float(tt.item())
+        t_var[gname] = t_v
     clocks = sampler.stop()
-    t_steps = [a.elapsed_time(b) * 1e-3 for a, b in ev_step]
-    t_step = sum(t_steps) / args.steps
+    gather_used = min(t_var, key=t_var.get)
+    t_step = t_var[gather_used]
+    step = variants[gather_used]
     # per-kernel split (same inputs, separate untimed-for-value loops) for the rooflines
     nk = min(args.steps, 50)
     ev_k1 = timed(lambda: act_quant_into(x, w.fmt, had, a.codes, a.sf, a.tensor_scale_dev, a.scratch), nk)
@@ -261,15 +299,11 @@ def main():
     torch.cuda.synchronize(dev)
     k1_mean = sum(a_.elapsed_time(b_) for a_, b_ in ev_k1) / nk * 1e-3
     k2_mean = sum(a_.elapsed_time(b_) for a_, b_ in ev_k2) / nk * 1e-3
-    if world > 1:
-        tt = torch.tensor([t_step], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_step = float(tt.item())
     flops = 2.0 * M * N * K  # whole job (all ranks together compute the full N)
     value = flops / t_step / 1e12
 
     # ---------------- cuBLAS bf16 of the same layer (primary comparator)
-    wb = w_dense if world == 1 else w_dense[rank * w.N:(rank + 1) * w.N]
+    wb = w_dense if not sharded else w_dense[rank * w.N:(rank + 1) * w.N]
     yb = torch.empty((M, wb.shape[0]), dtype=torch.bfloat16, device=dev)
     for _ in range(args.warmup):
         torch.matmul(x, wb.t(), out=yb)
@@ -294,7 +328,7 @@ def main():
         ne = min(args.steps, 20)
 
         def e2e_step():
-            if world > 1:
+            if sharded:
                 xd.copy_(xh, non_blocking=True)
                 yh.copy_(P.quantized_linear_sharded(xd, w), non_blocking=True)
             else:   # public host-buffer API: H2D, K1 + K2 and D2H pipelined over row chunks
@@ -310,7 +344,7 @@ def main():
         e1.record(stream)
         barrier()
         t_e2e = e0.elapsed_time(e1) * 1e-3 / ne
-        if world > 1:
+        if sharded:
             tt = torch.tensor([t_e2e], device=dev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             t_e2e = float(tt.item())
@@ -319,7 +353,7 @@ def main():
                "d2h_bytes_per_step": yh.numel() * yh.element_size()}
 
     if rank != 0:
-        if world > 1:
+        if sharded:
             dist.destroy_process_group()
         return
 
@@ -368,11 +402,15 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
-        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "fp4-e2m1 (fp32 accum)",
+        "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "fp4-e2m1 (fp32 accum)",
         "data": "synthetic: bf16 N(0,1) activations, N(0,1/K) random-init weights (GPU RTN)",
         "config": {"workload": name, "M": M, "K": K, "N": N, "format": fmt, "hadamard": had,
-                   "parallelism": f"N-shard x{world}" if world > 1 else "single", "l2": "flushed between steps (256 MiB memset + 256 MiB read sweep)"},
+                   "parallelism": f"N-shard x{world}" if sharded else "single",
+                   "gather": gather_used if sharded else None,
+                   "l2": "flushed between steps (256 MiB memset + 256 MiB read sweep)"},
         "k1_us": k1_mean * 1e6, "k2_us": k2_mean * 1e6,
+        "gather_ms_per_step": {k_: v_ * 1e3 for k_, v_ in t_var.items()} if sharded else None,
+        "gemm_tflops_per_gpu": k2_flops / k2_mean / 1e12,
         "rotquant_gbs": k1_bytes / k1_mean / 1e9,
         "bf16_cublas_us": t_bf16 * 1e6, "bf16_cublas_tflops": 2.0 * M * wb.shape[0] * K / t_bf16 / 1e12,
         "speedup_vs_cublas_bf16": t_bf16 / t_step,
@@ -383,7 +421,7 @@ def main():
         "gpu_launches": launches_per_step * args.steps,
     }
     print(json.dumps(line), flush=True)
-    if world > 1:
+    if sharded:
         dist.destroy_process_group()
 
 
