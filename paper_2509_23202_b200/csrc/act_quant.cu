@@ -1348,7 +1348,7 @@ int knob(const char* name, int dflt) {
 int num_sms() { return device_sms(); }
 
 // One CTA set per SM that the occupancy calculator allows (cached per kernel and device).
-template <auto Kern, int NW>
+template <auto Kern, int NW, bool kCoop = false>
 int launch_persistent(int smem, const CUtensorMap& tm, const AQParams& p, cudaStream_t s) {
   static std::atomic<int> cache[kMaxDevices];
   const int per_sm = per_device_once(cache, [&] {
@@ -1363,7 +1363,7 @@ int launch_persistent(int smem, const CUtensorMap& tm, const AQParams& p, cudaSt
   if (per_sm < 0) return MRFP4_ECUDA;
   const int64_t need = ceil_div(p.items, NW);
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)per_sm * num_sms()));
-  return launch_pdl(Kern, dim3(grid), dim3(NW * 32), smem, s, tm, p) == cudaSuccess ? MRFP4_OK : MRFP4_ECUDA;
+  return launch_pdl(Kern, dim3(grid), dim3(NW * 32), smem, s, kCoop, tm, p) == cudaSuccess ? MRFP4_OK : MRFP4_ECUDA;
 }
 
 // FlatWalk's TMA view of X: [total_segs rows][one segment = kLaneBytes] bytes, box = one
@@ -1388,8 +1388,8 @@ int launch_nw(const AQParams& p, const CUtensorMap& tm, cudaStream_t s) {
   constexpr int smem = InCfg<IN>::smem(NW);
   if constexpr (FMT == MRFP4_FMT_NVFP4) {
     if (!p.static_ts) {
-      if (p.nseg) return launch_persistent<k_act_quant_nv<IN, HK, FlatWalk, NW>, NW>(smem, tm, p, s);
-      return launch_persistent<k_act_quant_nv<IN, HK, GenWalk, NW>, NW>(smem, tm, p, s);
+      if (p.nseg) return launch_persistent<k_act_quant_nv<IN, HK, FlatWalk, NW>, NW, true>(smem, tm, p, s);
+      return launch_persistent<k_act_quant_nv<IN, HK, GenWalk, NW>, NW, true>(smem, tm, p, s);
     }
   }
   if (p.nseg) return launch_persistent<k_act_quant_1p<IN, FMT, HK, FlatWalk, NW>, NW>(smem, tm, p, s);
@@ -1405,7 +1405,7 @@ int launch_mma_cfg(AQParams p, cudaStream_t s) {
   p.items = ceil_div((int64_t)p.total_segs, 32 * U);
   constexpr int smem = mring_smem<U, S, NW>();
   if constexpr (FMT == MRFP4_FMT_NVFP4) {
-    if (!p.static_ts) return launch_persistent<k_act_quant_nv_mma<IN, HK, U, S, NW, MB>, NW>(smem, tm, p, s);
+    if (!p.static_ts) return launch_persistent<k_act_quant_nv_mma<IN, HK, U, S, NW, MB>, NW, true>(smem, tm, p, s);
   }
   return launch_persistent<k_act_quant_1p_mma<IN, FMT, HK, U, S, NW, MB>, NW>(smem, tm, p, s);
 }

@@ -88,21 +88,40 @@ inline int per_device_once(std::atomic<int> (&slot)[kMaxDevices], F&& init) {
 }
 
 // Launch `kern` on `s` with the PDL attribute (disabled when MRFP4_PDL=0 in the environment).
+// `cooperative`: the kernel spin-waits on other CTAs of its grid (the NVFP4 act-quant grid
+// barrier, the split-K GEMM's in-kernel reduction), so the launch must guarantee that every
+// CTA is co-resident -- under MPS, green contexts or a concurrent persistent kernel it then
+// fails (cudaErrorCooperativeLaunchTooLarge -> MRFP4_ECUDA) instead of hanging.  If the driver
+// refuses the cooperative + PDL combination, it is retried cooperative only.
 bool pdl_enabled();
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
-                       Args&&... args) {
+                       bool cooperative, Args&&... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[2];
+  int n = 0;
+  if (pdl_enabled()) {
+    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[n++].val.programmaticStreamSerializationAllowed = 1;
+  }
+  if (cooperative) {
+    attr[n].id = cudaLaunchAttributeCooperative;
+    attr[n++].val.cooperative = 1;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+  cfg.numAttrs = n;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, args...);
+  if (e != cudaSuccess && cooperative && n == 2 && e != cudaErrorCooperativeLaunchTooLarge) {
+    (void)cudaGetLastError();
+    attr[0] = attr[1];
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, kern, args...);
+  }
+  return e;
 }
 
 }  // namespace mrfp4

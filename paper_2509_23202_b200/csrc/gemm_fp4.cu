@@ -24,6 +24,7 @@
 #include <type_traits>
 #include <cstring>
 #include <mutex>
+#include <unordered_map>
 
 #include "common.cuh"
 #include "quant_core.cuh"
@@ -987,7 +988,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<VEC>::kThreads2
 extern int g_force_grid;
 namespace {
 
-PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
+PFN_cuTensorMapEncodeTiled_v12000 driver_encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
   std::call_once(once, [] {
@@ -998,6 +999,60 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
       fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
   });
   return fn;
+}
+
+// Tensor maps are pure functions of their arguments (address, shape, box, swizzle): a launch
+// re-using the buffers of an earlier one (every decode step, every layer of a model) gets the
+// same 128-B descriptor from this cache instead of re-encoding it on the host.  Bounded
+// (cleared past 4096 entries), mutex-guarded.
+struct MapKey {
+  uint64_t w[20];
+  bool operator==(const MapKey& o) const { return memcmp(w, o.w, sizeof(w)) == 0; }
+};
+struct MapKeyHash {
+  size_t operator()(const MapKey& k) const {
+    uint64_t h = 1469598103934665603ull;
+    for (uint64_t v : k.w) h = (h ^ v) * 1099511628211ull;
+    return (size_t)h;
+  }
+};
+
+CUresult cached_encode(CUtensorMap* tm, CUtensorMapDataType dt, cuuint32_t rank, void* addr, const cuuint64_t* dims,
+                       const cuuint64_t* strides, const cuuint32_t* box, const cuuint32_t* estr,
+                       CUtensorMapInterleave il, CUtensorMapSwizzle sw, CUtensorMapL2promotion l2,
+                       CUtensorMapFloatOOBfill oob) {
+  static std::mutex mu;
+  static std::unordered_map<MapKey, CUtensorMap, MapKeyHash> cache;
+  if (rank < 1 || rank > 3) return driver_encode_fn()(tm, dt, rank, addr, dims, strides, box, estr, il, sw, l2, oob);
+  MapKey k{};
+  k.w[0] = (uint64_t)dt | ((uint64_t)rank << 8) | ((uint64_t)il << 16) | ((uint64_t)sw << 24) | ((uint64_t)l2 << 32) |
+           ((uint64_t)oob << 40);
+  k.w[1] = reinterpret_cast<uint64_t>(addr);
+  for (cuuint32_t i = 0; i < rank; ++i) {
+    k.w[2 + i] = dims[i];
+    k.w[5 + i] = i + 1 < rank ? strides[i] : 0;
+    k.w[8 + i] = box[i];
+    k.w[11 + i] = estr[i];
+  }
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(k);
+    if (it != cache.end()) {
+      *tm = it->second;
+      return CUDA_SUCCESS;
+    }
+  }
+  const CUresult r = driver_encode_fn()(tm, dt, rank, addr, dims, strides, box, estr, il, sw, l2, oob);
+  if (r == CUDA_SUCCESS) {
+    std::lock_guard<std::mutex> lock(mu);
+    if (cache.size() > 4096) cache.clear();
+    cache.emplace(k, *tm);
+  }
+  return r;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
+  return driver_encode_fn() ? &cached_encode : nullptr;
 }
 
 }  // namespace
@@ -1092,7 +1147,9 @@ int launch(const uint8_t* a, const uint8_t* b, const GemmArgs& args0, cudaStream
   const int units = tiles * g.splits;
   int grid = std::min(units, num_sms());
   if (g_force_grid > 0) grid = std::min(grid, g_force_grid);
-  if (launch_pdl(k_gemm_fp4<VEC, BN, OUT>, dim3(grid), dim3(kThreads), C::kSmem, s, tmA, tmB, g) != cudaSuccess)
+  // split-K reduces inside the kernel (every split waits for its tile's others): co-residency
+  if (launch_pdl(k_gemm_fp4<VEC, BN, OUT>, dim3(grid), dim3(kThreads), C::kSmem, s, g.splits > 1, tmA, tmB, g) !=
+      cudaSuccess)
     return MRFP4_ECUDA;
   return MRFP4_OK;
 }
@@ -1122,7 +1179,7 @@ int launch2(const uint8_t* a, const uint8_t* b, const GemmArgs& args0, cudaStrea
   const int tiles = g.num_m_blk * g.num_n_blk;
   int nclu = std::min(tiles, num_sms() / 2);
   if (g_force_grid > 0) nclu = std::min(nclu, std::max(1, g_force_grid / 2));
-  return launch_pdl(k_gemm_fp4_2sm<VEC, OUT, HKQ>, dim3(2 * nclu), dim3(C::kThreads2), C::kSmem, s, tmA, tmB, tmSfa,
+  return launch_pdl(k_gemm_fp4_2sm<VEC, OUT, HKQ>, dim3(2 * nclu), dim3(C::kThreads2), C::kSmem, s, false, tmA, tmB, tmSfa,
                     tmSfb, g) ==
                  cudaSuccess
              ? MRFP4_OK
