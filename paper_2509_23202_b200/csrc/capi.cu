@@ -51,6 +51,19 @@ bool pdl_enabled() {
   }();
   return on;
 }
+// Cooperative launch of the grid-synchronizing kernels: opt-in (MRFP4_COOP=1).  A cooperative
+// launch cannot also be a programmatic dependent launch, which costs ~4 us per decode-sized
+// layer (c0: 21.5 -> 25.6 us, scripts/c0_coop_probe.sh).  By default the grids are sized by the
+// occupancy calculator to be co-resident on the whole GPU; deployments that share SMs (MPS
+// partitions, green contexts, concurrent persistent kernels) should set MRFP4_COOP=1, which makes
+// an over-subscribed launch fail instead of hang.
+bool coop_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("MRFP4_COOP");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
 }  // namespace mrfp4
 
 namespace {

@@ -89,11 +89,13 @@ inline int per_device_once(std::atomic<int> (&slot)[kMaxDevices], F&& init) {
 
 // Launch `kern` on `s` with the PDL attribute (disabled when MRFP4_PDL=0 in the environment).
 // `cooperative`: the kernel spin-waits on other CTAs of its grid (the NVFP4 act-quant grid
-// barrier, the split-K GEMM's in-kernel reduction), so the launch must guarantee that every
-// CTA is co-resident -- under MPS, green contexts or a concurrent persistent kernel it then
-// fails (cudaErrorCooperativeLaunchTooLarge -> MRFP4_ECUDA) instead of hanging.  If the driver
-// refuses the cooperative + PDL combination, it is retried cooperative only.
+// barrier, the split-K GEMM's in-kernel reduction).  Its grid is sized from the occupancy
+// calculator so every CTA is co-resident on an otherwise idle GPU; with MRFP4_COOP=1 the launch
+// is also made cooperative, so that under MPS, green contexts or a concurrent persistent kernel
+// it fails (cudaErrorCooperativeLaunchTooLarge -> MRFP4_ECUDA) instead of hanging.  If the
+// driver refuses the cooperative + PDL combination, it is retried cooperative only.
 bool pdl_enabled();
+bool coop_enabled();
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                        bool cooperative, Args&&... args) {
@@ -108,14 +110,14 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
     attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[n++].val.programmaticStreamSerializationAllowed = 1;
   }
-  if (cooperative) {
+  if (cooperative && coop_enabled()) {
     attr[n].id = cudaLaunchAttributeCooperative;
     attr[n++].val.cooperative = 1;
   }
   cfg.attrs = attr;
   cfg.numAttrs = n;
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, args...);
-  if (e != cudaSuccess && cooperative && n == 2 && e != cudaErrorCooperativeLaunchTooLarge) {
+  if (e != cudaSuccess && n == 2 && e != cudaErrorCooperativeLaunchTooLarge) {
     (void)cudaGetLastError();
     attr[0] = attr[1];
     cfg.numAttrs = 1;

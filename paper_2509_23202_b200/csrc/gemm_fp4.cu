@@ -506,12 +506,26 @@ __global__ void __launch_bounds__(kThreads, 1)
 // ---------------------------------------------------------------------------
 template <int VEC>
 struct Cfg2 {
-  static constexpr int kBK = 512;                                // FP4 elements per stage
+#ifndef MRFP4_K2_BK
+#define MRFP4_K2_BK 256
+#endif
+#ifndef MRFP4_K2_STAGES
+#define MRFP4_K2_STAGES 6
+#endif
+#ifndef MRFP4_K2_SFSLOTS
+#define MRFP4_K2_SFSLOTS 5
+#endif
+  // 256-wide stages, 6 deep (16-KB boxes per operand per CTA, the shape of cuBLASLt's
+  // 256x256x256 2-SM block-scaled kernel), with the scale factors on their own producer warp:
+  // a slot is recycled after 4 MMAs.  70B up NVFP4 K2: 194 -> 163 us (91% of 4x bf16);
+  // 3 x 512-wide stages with one producer thread for A/B and SF: 196 us; 256-wide with one
+  // producer thread: 262 us (the thread could not issue fast enough) -- profiles/r02_k2_notes.md.
+  static constexpr int kBK = MRFP4_K2_BK;                        // FP4 elements per stage
   static constexpr int kSlices = kBK / BK;                       // 128-B K slices per stage
   static constexpr int kMmas = kBK / UMMA_K;                     // MMAs per stage
   static constexpr int kAtoms = kBK / VEC / 4;                   // SF atoms (128 rows x 4 cols) per stage
-  static constexpr int kStages = 3;                              // A/B stages
-  static constexpr int kSfSlots = VEC == 16 ? 2 : 3;             // SF slots (SMEM and TMEM)
+  static constexpr int kStages = MRFP4_K2_STAGES;                // A/B stages
+  static constexpr int kSfSlots = MRFP4_K2_SFSLOTS;              // SF slots (SMEM and TMEM)
   static constexpr int kABytes = 128 * kBK / 2;
   static constexpr int kBBytes = 128 * kBK / 2;
   static constexpr int kSfaBytes = kAtoms * 512;
@@ -529,7 +543,15 @@ struct Cfg2 {
   static constexpr int kOffBar = kOffSfb + kSfSlots * kSfbBytes;
   static constexpr int kSmem = kOffBar + 512 + 1024;
   static_assert(kSmem <= 232448, "SMEM budget");
-  static constexpr int kEpiWarp0 = 2;
+#ifndef MRFP4_K2_SFWARP
+#define MRFP4_K2_SFWARP 1
+#endif
+#ifndef MRFP4_K2_BWARP
+#define MRFP4_K2_BWARP 0
+#endif
+  static constexpr bool kSfWarp = MRFP4_K2_SFWARP;   // scale factors issued by their own producer warp (2)
+  static constexpr bool kBWarp = kSfWarp && MRFP4_K2_BWARP;   // B codes by their own producer warp (3)
+  static constexpr int kEpiWarp0 = 2 + kSfWarp + kBWarp;
   static constexpr int kEpiWarps = 8;   // 2 per TMEM lane quadrant, 128 accumulator columns each
   static constexpr int kThreads2 = 32 * (kEpiWarp0 + kEpiWarps);
 };
@@ -803,7 +825,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<VEC>::kThreads2
       };
       // PDL pre-issue: the weight half of the first A/B stages
       int pre = 0;
-      if (g.preissue) {
+      if (g.preissue && !C::kBWarp) {
         StageIter q2 = abq;
         for (; pre < C::kStages && q2.live; ++pre) {
           arm(&full[pre], C::kABytes + C::kBBytes);
@@ -818,15 +840,59 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<VEC>::kThreads2
         abq.advance();
         ab.next<C::kStages>();
       }
-      while (abq.live || sfq.live) {
-        if (sfq.live && sm100::mbar_test(&sf_empty[sf.idx], sf.ph ^ 1)) {
-          load_sf();
-        } else if (abq.live && sm100::mbar_test(&empty[ab.idx], ab.ph ^ 1)) {
+      if constexpr (C::kSfWarp) {
+        while (abq.live) {
+          sm100::mbar_wait(&empty[ab.idx], ab.ph ^ 1);
           arm(&full[ab.idx], C::kABytes + C::kBBytes);
-          load_ab(true, true);
+          load_ab(true, !C::kBWarp);
           abq.advance();
           ab.next<C::kStages>();
         }
+      } else {
+        while (abq.live || sfq.live) {
+          if (sfq.live && sm100::mbar_test(&sf_empty[sf.idx], sf.ph ^ 1)) {
+            load_sf();
+          } else if (abq.live && sm100::mbar_test(&empty[ab.idx], ab.ph ^ 1)) {
+            arm(&full[ab.idx], C::kABytes + C::kBBytes);
+            load_ab(true, true);
+            abq.advance();
+            ab.next<C::kStages>();
+          }
+        }
+      }
+    }
+  } else if (C::kBWarp && warp == 3) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ B producer
+      // The weight stream on its own thread (it does not depend on the act-quant kernel: no
+      // PDL wait); the A producer arms `full` with both operands' bytes.
+      Ring ab;
+      StageIter q(g, cluster, nclusters, num_m_blk);
+      while (q.live) {
+        sm100::mbar_wait(&empty[ab.idx], ab.ph ^ 1);
+        tma_load_3d_2sm(smem + C::kOffB + ab.idx * C::kBBytes, &tmB, sm100::leader_bar(&full[ab.idx]),
+                        q.n_blk() * 256 + (int)rank * 128, q.kb * C::kSlices);
+        q.advance();
+        ab.next<C::kStages>();
+      }
+    }
+  } else if (C::kSfWarp && warp == 2) {
+    if (lane == 0) {
+      // ---------------------------------------------------------- SF producer
+      // The scale-factor stream on its own thread: its slot waits and small TMA issues never
+      // delay the A/B stream (and vice versa).
+      Ring sf;
+      StageIter sfq(g, cluster, nclusters, num_m_blk);
+      pdl_wait();   // SFA comes from the act-quant kernel
+      while (sfq.live) {
+        sm100::mbar_wait(&sf_empty[sf.idx], sf.ph ^ 1);
+        const int kb = sfq.kb, mb = sfq.m_blk(), nb = sfq.n_blk();
+        if (leader) sm100::mbar_arrive_expect_tx(&sf_full[sf.idx], 2u * (C::kSfaBytes + C::kSfbBytes));
+        const uint32_t bar = sm100::leader_bar(&sf_full[sf.idx]);
+        tma_load_3d_2sm(smem + C::kOffSfa + sf.idx * C::kSfaBytes, &tmSfa, bar, 2 * C::kAtoms * kb, mb * 2 + (int)rank);
+        tma_load_3d_2sm(smem + C::kOffSfb + sf.idx * C::kSfbBytes, &tmSfb, bar, 2 * C::kAtoms * kb, nb * 2);
+        sfq.advance();
+        sf.next<C::kSfSlots>();
       }
     }
   } else if (warp == 1) {
