@@ -42,6 +42,8 @@ CONFIGS = {
     "c0": ("llama3-8b attn.q_proj 4096->4096, 16 tokens, NVFP4+H16", 16, 4096, 4096, "nvfp4", 16),
     "c2-up-nv": ("llama3-70b mlp.up 8192->28672, 2048 tokens, NVFP4+H16", 2048, 8192, 28672, "nvfp4", 16),
     "c2-down-mx": ("llama3-70b mlp.down 28672->8192, 2048 tokens, MXFP4+H32", 2048, 28672, 8192, "mxfp4", 32),
+    "c2-up-mx": ("llama3-70b mlp.up 8192->28672, 2048 tokens, MXFP4+H32", 2048, 8192, 28672, "mxfp4", 32),
+    "c2-down-nv": ("llama3-70b mlp.down 28672->8192, 2048 tokens, NVFP4+H16", 2048, 28672, 8192, "nvfp4", 16),
     "c3-gateup": ("qwen3-32b mlp.gate_up 5120->51200, 2048 tokens, NVFP4+H128", 2048, 5120, 51200, "nvfp4", 128),
     "c4": ("llama3-405b-shaped mlp 16384->53248, 8192 tokens, NVFP4+H16", 8192, 16384, 53248, "nvfp4", 16),
 }
