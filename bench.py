@@ -233,7 +233,18 @@ def main():
             gathers = [gg for gg in gathers if gg != "fused"] or ["nccl"]
     cols = slice(rank * w.N, (rank + 1) * w.N)
 
+    # Decode-sized layers (M <= 32) run as ONE kernel: the act-quant inside the GEMM CTAs
+    # (mrfp4_linear_decode), which is what quantized_linear launches for them.
+    from paper_2509_23202_b200.linear import _linear_decode, decode_eligible, decode_workspace_bytes
+    fused_decode = not sharded and decode_eligible(M, w, x.dtype) and os.environ.get("MRFP4_DECODE", "1") != "0"
+    if fused_decode:
+        launches_per_step = 1
+        dws = torch.zeros(max(decode_workspace_bytes(M, w), 1), dtype=torch.uint8, device=dev)
+
     def step_nccl():
+        if fused_decode:
+            _linear_decode(x, w, y, dws, None)
+            return
         act_quant_into(x, w.fmt, had, a.codes, a.sf, a.tensor_scale_dev, a.scratch)
         P.gemm(a, w, y)
         if sharded:
@@ -298,9 +309,12 @@ def main():
     nk = min(args.steps, 50)
     ev_k1 = timed(lambda: act_quant_into(x, w.fmt, had, a.codes, a.sf, a.tensor_scale_dev, a.scratch), nk)
     ev_k2 = timed(lambda: P.gemm(a, w, y), nk)
+    if fused_decode:   # the one kernel of the step (K1 and K2 above: the two-kernel path, for reference)
+        ev_kd = timed(step_nccl, nk)
     torch.cuda.synchronize(dev)
     k1_mean = sum(a_.elapsed_time(b_) for a_, b_ in ev_k1) / nk * 1e-3
     k2_mean = sum(a_.elapsed_time(b_) for a_, b_ in ev_k2) / nk * 1e-3
+    kd_mean = sum(a_.elapsed_time(b_) for a_, b_ in ev_kd) / nk * 1e-3 if fused_decode else None
     flops = 2.0 * M * N * K  # whole job (all ranks together compute the full N)
     value = flops / t_step / 1e12
 
@@ -391,7 +405,14 @@ def main():
         cpu = {"value": 2.0 * Ms * N * K / tc / 1e12, "unit": "TFLOP/s", "cores": cores, "kind": "port",
                "sample": f"M={Ms} of {M} tokens, act-quant + dequant + fp32 matmul, {reps} reps"}
 
-    if k2_hbm_bound:
+    if fused_decode:   # the step's one kernel: weight-stream bound (W codes + scales, X in, Y out)
+        kd_bytes = k2_bytes + 2.0 * M * K + 4
+        k2_roof = {"bound": "hbm", "kernel": "k_linear_decode (K1 + K2 in one launch)",
+                   "achieved": kd_bytes / kd_mean / 1e9, "peak": hbm, "unit": "GB/s",
+                   "frac": kd_bytes / kd_mean / 1e9 / hbm,
+                   "note": f"{kd_bytes / 1e6:.2f} MB algorithmic (W codes and scales, bf16 X in, bf16 Y out) per launch",
+                   "us": kd_mean * 1e6, "traffic": traffic}
+    elif k2_hbm_bound:
         k2_roof = {"bound": "hbm", "kernel": "k_gemm_fp4 (K2)", "achieved": k2_bytes / k2_mean / 1e9,
                    "peak": hbm, "unit": "GB/s", "frac": k2_bytes / k2_mean / 1e9 / hbm,
                    "note": f"{k2_bytes / 1e6:.2f} MB algorithmic (A + W codes and scales, bf16 out) per launch",

@@ -228,6 +228,27 @@ int mrfp4_mse_pass(const double* y, int64_t ngroups, int fmt, const double* cand
 int mrfp4_mse_group_err(const double* y, int64_t ngroups, int fmt, const double* decoded, double ts,
                         double* group_err, uint32_t* status, void* stream);
 /*
+ * Decode-sized quantized linear in one kernel (M <= 32 tokens): the activation rotate +
+ * quantize of mrfp4_act_quant runs inside the GEMM CTAs (each CTA reduces the NVFP4 global
+ * scale over the whole, tiny, activation itself -- no grid barrier), and the FP4 GEMM puts the
+ * weight on the 128-row MMA side (D^T = W . Xq^T, N = 16 | 32 tokens).  Same result as
+ * mrfp4_act_quant + mrfp4_gemm up to fp32 summation order.  x: [M, K] contiguous bf16 / f16;
+ * w: [N, K/2] codes + swizzled scales + device tensor scale; d: [M, N] (row stride ldd) bf16 /
+ * f32.  One thread-block cluster per 128-row weight tile, its CTAs splitting K (<= 8): the
+ * NVFP4 whole-tensor max and the K-split partial sums are combined over distributed shared
+ * memory, so no workspace and no grid-wide synchronization is involved.  Requires K % 256 == 0,
+ * N % 128 == 0, had_k in {0, 16, 32}, M * K <= 2^18 and a slice of <= 16K elements per CTA;
+ * returns MRFP4_EUNSUPPORTED otherwise (use mrfp4_act_quant + mrfp4_gemm).  workspace: unused
+ * (mrfp4_linear_decode_workspace() returns 0).  status: optional device word for the DataError bits.
+ */
+size_t mrfp4_linear_decode_workspace(int64_t M, int64_t N, int64_t K);
+/* CTAs mrfp4_linear_decode launches for this shape (0: not a decode shape it takes). */
+int mrfp4_linear_decode_ctas(int64_t M, int64_t N, int64_t K);
+int mrfp4_linear_decode(const void* x, int x_dtype, int64_t M, int64_t K, int fmt, int had_k, const uint8_t* w,
+                        const uint8_t* w_sf, const float* w_ts, int64_t N, void* d, int d_dtype, int64_t ldd,
+                        void* workspace, size_t workspace_bytes, uint32_t* status, void* stream);
+
+/*
  * GPTQ column solver, one lazy block (replaces the inner loop of
  * _gptq_core, gptq.py:148-167): for columns i1 .. i1+block-1 (block <= 128) of the permuted
  * weight W [rows, d] (float64, row-major, updated in place), column scales S [rows, d] and the

@@ -56,6 +56,10 @@ SIGNATURES = {
     "mrfp4_mse_group_err": (_int, [_vp, _i64, _int, _vp, _c.c_double, _vp, _vp, _vp]),
     "mrfp4_gemm_peers": (_int, [_vp, _vp, _vp, _vp, _vp, _vp, _c.POINTER(_vp), _int, _i64, _i64, _i64, _i64, _int,
                                 _vp]),
+    "mrfp4_linear_decode_workspace": (_sz, [_i64, _i64, _i64]),
+    "mrfp4_linear_decode_ctas": (_int, [_i64, _i64, _i64]),
+    "mrfp4_linear_decode": (_int, [_vp, _int, _i64, _i64, _int, _int, _vp, _vp, _vp, _i64, _vp, _int, _i64, _vp, _sz,
+                                   _vp, _vp]),
     "mrfp4_gptq_block": (_int, [_vp, _vp, _vp, _i64, _i64, _int, _int, _vp, _vp, _vp, _vp]),
     "mrfp4_pairwise_sums": (_int, [_vp, _vp, _vp, _i64, _vp, _vp]),
 }

@@ -13,6 +13,11 @@ namespace mrfp4 {
 int launch_act_quant(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ldx, int fmt, int hk, uint8_t* codes,
                      uint8_t* sf, float* tensor_scale, uint32_t* status, void* workspace,
                      const mrfp4_act_quant_opts* opts, cudaStream_t s);
+int launch_linear_decode(const void* x, int x_dtype, int64_t M, int64_t K, int fmt, int hk, const uint8_t* w,
+                         const uint8_t* w_sf, const float* w_ts, int64_t N, void* d, int d_dtype, int64_t ldd,
+                         void* ws, size_t ws_bytes, uint32_t* status, cudaStream_t s);
+size_t decode_workspace_bytes(int64_t M, int64_t N, int64_t K);
+bool decode_plan(int64_t M, int64_t N, int64_t K, int* splits, int* kb_per);
 int launch_gptq_block(double* W, const double* S, const double* T, int64_t rows, int64_t d, int i1, int B, double* Q,
                       uint8_t* codes, double* Err, cudaStream_t s);
 int launch_rotate_f64(const double* x, int64_t M, int64_t K, int64_t ldx, int hk, double* y, cudaStream_t s);
@@ -155,6 +160,35 @@ int mrfp4_rotate_f64(const double* x, int64_t M, int64_t K, int64_t ldx, int had
   if (ldx < K || !x || !y) return fail(MRFP4_EINVAL, "bad arguments");
   return cuda_status(mrfp4::launch_rotate_f64(x, M, K, ldx, had_k, y, static_cast<cudaStream_t>(stream)),
                      "mrfp4_rotate_f64");
+}
+
+int mrfp4_linear_decode_ctas(int64_t M, int64_t N, int64_t K) {
+  if (M < 1 || M > 32 || K % 256 || K < 256 || N % 128 || M * K > (1 << 18)) return 0;
+  int sp, per;
+  if (!mrfp4::decode_plan(M, N, K, &sp, &per)) return 0;
+  return (int)(N / 128) * sp;
+}
+
+size_t mrfp4_linear_decode_workspace(int64_t M, int64_t N, int64_t K) {
+  if (M < 1 || M > 32 || K % 256 || N % 128) return 0;
+  return mrfp4::decode_workspace_bytes(M, N, K);
+}
+
+int mrfp4_linear_decode(const void* x, int x_dtype, int64_t M, int64_t K, int fmt, int had_k, const uint8_t* w,
+                        const uint8_t* w_sf, const float* w_ts, int64_t N, void* d, int d_dtype, int64_t ldd,
+                        void* workspace, size_t workspace_bytes, uint32_t* status, void* stream) {
+  if (mrfp4_group_size(fmt) == 0) return fail(MRFP4_EUNSUPPORTED, "unknown format %d", fmt);
+  if (!x || !w || !w_sf || !w_ts || !d) return fail(MRFP4_EINVAL, "null buffer");
+  if (d_dtype != MRFP4_DT_BF16 && d_dtype != MRFP4_DT_F32) return fail(MRFP4_EUNSUPPORTED, "output dtype");
+  if (ldd < N) return fail(MRFP4_EINVAL, "bad output row stride");
+  if (!aligned(x, 16) || !aligned(w, 16) || !aligned(w_sf, 16))
+    return fail(MRFP4_EUNSUPPORTED, "buffers must be 16-byte aligned");
+  const int rc = mrfp4::launch_linear_decode(x, x_dtype, M, K, fmt, had_k, w, w_sf, w_ts, N, d, d_dtype, ldd,
+                                             workspace, workspace_bytes, status, static_cast<cudaStream_t>(stream));
+  if (rc == MRFP4_EUNSUPPORTED)
+    return fail(MRFP4_EUNSUPPORTED, "not a decode shape (M <= 32, K %% 256 == 0, N %% 128 == 0, k <= 32, "
+                                    "M * K <= 2^18, M * K / 8 splits <= 16K elements, bf16 / f16 input)");
+  return cuda_status(rc, "mrfp4_linear_decode");
 }
 
 int mrfp4_gptq_block(double* W, const double* S, const double* T, int64_t rows, int64_t d, int i1, int block,

@@ -1,0 +1,556 @@
+// Decode-sized quantized linear in ONE kernel (M <= 32 tokens): the activation rotate + FP4
+// quantize (K1) runs inside the GEMM CTAs, and the GEMM puts the WEIGHT on the 128-row side of
+// the MMA (D^T[128 weight rows, 16 | 32 tokens] = W_tile . Xq^T), so a 16-token batch does not
+// waste a 128-row MMA tile.  Replaces quantize_rtn(X) -> dequantize(Aq) @ dequantize(Wq).T
+// (/root/reference/pkg/src/microfp/quantizers.py:247-255, formats.py:424-442) at decode sizes,
+// where the two-kernel path (K1 with its grid barrier, then split-K K2) is a chain of launch and
+// round-trip latencies rather than bandwidth (c0: 21.5 us vs cuBLAS bf16's 14.6 us).
+//
+// One CLUSTER per 128-row weight tile; its CTAs split K (cluster size = splits <= 8), so a
+// cluster sees the whole activation and every exchange is over distributed shared memory:
+//   1. warp 0 issues the CTA's first weight stages (TMA codes + scale-factor atoms) at once --
+//      the weight does not depend on the predecessor kernel -- so the weight stream (the only
+//      real traffic at decode) overlaps everything below;
+//   2. each CTA rotates its K-slice of every token and, for NVFP4, reduces max |X H| over it;
+//      the cluster combines the slices' maxima over DSMEM -- the whole-tensor max, identical in
+//      every cluster, so the global scale s_T (quantizers.py:195-200) needs no grid barrier;
+//   3. the CTA quantizes its slice (quant_core.cuh: the K1 arithmetic, bit-exact with
+//      mrfp4_act_quant) straight into shared memory, in the MMA's K-major 128-B-swizzled operand
+//      layout plus 128x4 scale-factor atoms (rows >= M zero);
+//   4. one thread issues tcgen05.cp (scale factors) + tcgen05.mma kind::mxf4nvf4 M=128, N=16|32,
+//      K=64 per stage into a TMEM accumulator;
+//   5. the epilogue moves the CTA's fp32 partial D^T into shared memory; after a cluster barrier
+//      CTA r sums rows [r * 128 / S, (r + 1) * 128 / S) of all S partials in rank order over
+//      DSMEM (deterministic), scales by ts_x * ts_w and stores Y[m, n] (coalesced over n).
+// No global workspace, no atomics, no CTA waits on another cluster.
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstring>
+
+#include "common.cuh"
+#include "quant_core.cuh"
+#include "sm100.cuh"
+
+namespace mrfp4 {
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder();  // gemm_fp4.cu (cached encoder)
+
+namespace {
+using namespace qc;
+
+#ifndef MRFP4_DEC_THREADS
+#define MRFP4_DEC_THREADS 256
+#endif
+constexpr int kDecThreads = MRFP4_DEC_THREADS;   // all quantize X; w0 producer, w1 MMA, w4-7 epilogue
+constexpr int kDecSegsPerCta = 512;              // 32-element activation segments one CTA rotates
+constexpr int kDecSegs = kDecSegsPerCta / kDecThreads;   // per thread, all loads in flight at once
+constexpr int kDecStages = 6;      // weight ring: 256-wide K stages
+constexpr int kDecStageCodes = 128 * 128;          // 128 weight rows x 128 B (256 FP4)
+constexpr int kDecMaxSliceStages = 16;             // <= 4096 K per CTA
+constexpr int kDecXStage = 32 * 128;               // X codes per stage: 32 token rows x 128 B
+constexpr int kDecMaxSplits = 8;                   // portable cluster size
+
+struct DecArgs {
+  const void* x;
+  int M, K, N, NT;          // NT: MMA N (tokens padded to 16 / 32)
+  int64_t ldd;
+  int fmt, hk;
+  const uint8_t* w_sf;
+  const float* w_ts;
+  void* d;
+  int out_f32;
+  int row_tiles, splits, kb_per, num_kb;
+  int64_t sf_col_blocks;    // weight / activation SF column blocks: ceil(K / G / 4)
+  uint32_t* status;
+  AQParams qp;              // c64 / kraw / kmx / pm / mx_ts of the activation quantization
+  double c6;                  // RN64(c64 / 6)
+  unsigned long long* trace;  // perf experiments: per-CTA globaltimer stamps (null in production)
+};
+unsigned long long* g_dec_trace = nullptr;
+
+template <int VEC>
+struct DecCfg {
+  static constexpr int kAtoms = 256 / VEC / 4;        // SF atoms (128 rows x 4 cols) per stage: 4 | 2
+  static constexpr int kSfStage = kAtoms * 512;       // bytes of one operand's SF per stage
+  static constexpr int kOffW = 0;
+  static constexpr int kOffWsf = kOffW + kDecStages * kDecStageCodes;
+  static constexpr int kOffX = kOffWsf + kDecStages * kSfStage;
+  static constexpr int kOffXsf = kOffX + kDecMaxSliceStages * kDecXStage;
+  static constexpr int kOffPart = kOffXsf + kDecMaxSliceStages * kSfStage;   // [32 tokens][128] fp32 partial
+  static constexpr int kSmem = kOffPart + 32 * 128 * 4 + 1024;
+  static constexpr int kSfCols = 2 * kAtoms * 4;      // TMEM SF columns per stage (A + B)
+  static constexpr int kTmemCols = 512;               // 32 (accumulator) + 6 x 32 | 16 SF columns
+};
+
+__device__ __forceinline__ void tc_mma_fp4_if(uint32_t el, int vec, uint32_t d, uint64_t ad, uint64_t bd,
+                                              uint32_t idesc, uint32_t sfa, uint32_t sfb, uint32_t acc) {
+  if (vec == 16) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\tsetp.ne.b32 e, %7, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::mxf4nvf4.block_scale.scale_vec::4X [%0], %1, %2, %3, [%5], [%6], p;\n\t}" ::
+            "r"(d), "l"(ad), "l"(bd), "r"(idesc), "r"(acc), "r"(sfa), "r"(sfb), "r"(el)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\tsetp.ne.b32 e, %7, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::mxf4nvf4.block_scale.scale_vec::2X [%0], %1, %2, %3, [%5], [%6], p;\n\t}" ::
+            "r"(d), "l"(ad), "l"(bd), "r"(idesc), "r"(acc), "r"(sfa), "r"(sfb), "r"(el)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void tc_cp_if(uint32_t el, uint32_t taddr, uint64_t sdesc) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\tsetp.ne.b32 e, %2, 0;\n\t"
+      "@e tcgen05.cp.cta_group::1.32x128b.warpx4 [%0], %1;\n\t}" ::"r"(taddr),
+      "l"(sdesc), "r"(el)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_if(uint64_t* bar, uint32_t el) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\tsetp.ne.b32 e, %1, 0;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+          sm100::smem_u32(bar)),
+      "r"(el)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t dadd(uint64_t d, uint32_t x) { return d + x; }
+// Loads from the same shared-memory offset in CTA `rank` of the cluster.
+__device__ __forceinline__ uint32_t mapa_u32(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(sm100::smem_u32(p)), "r"(rank));
+  return r;
+}
+// Asynchronous remote stores into CTA `rank`'s shared memory, counted (bytes) on ITS mbarrier
+// at the same offset as `bar`: data + signal in one, no cluster-scope fence.
+__device__ __forceinline__ void st_async_u32(const void* dst, uint32_t v, const uint64_t* bar, uint32_t rank) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.u32 [%0], %1, [%2];" ::"r"(mapa_u32(dst, rank)),
+               "r"(v), "r"(mapa_u32(bar, rank))
+               : "memory");
+}
+// dst / bar: shared::cluster addresses (mapa_u32)
+__device__ __forceinline__ void st_async_v4(uint32_t dst, uint32_t a, uint32_t b, uint32_t c, uint32_t d,
+                                            uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+                   dst),
+               "r"(a), "r"(b), "r"(c), "r"(d), "r"(bar)
+               : "memory");
+}
+
+template <int IN, int VEC, int HK>
+__global__ void __launch_bounds__(kDecThreads, 1)
+    k_linear_decode(const __grid_constant__ CUtensorMap tmW, DecArgs g) {
+  using C = DecCfg<VEC>;
+  constexpr int FMT = VEC == 16 ? MRFP4_FMT_NVFP4 : MRFP4_FMT_MXFP4;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t full[kDecStages], empty[kDecStages], tfull, mbar_max, mbar_part;
+  __shared__ uint32_t tmem_holder, wmax[kDecThreads / 32], cmaxs[kDecMaxSplits];
+  __shared__ EncConsts sk;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = blockIdx.x / g.splits, split = (int)sm100::cluster_ctarank();   // cluster = one row tile
+  const int kb0 = split * g.kb_per, kb1 = min(g.num_kb, kb0 + g.kb_per), nst = kb1 - kb0;
+  auto stamp = [&](int i) {   // slots 0..15
+    if (g.trace && threadIdx.x == 0) g.trace[blockIdx.x * 16 + i] = globaltimer();
+  };
+  stamp(0);
+
+  if (warp == 0 && lane == 0) {
+    sm100::tma_prefetch_desc(&tmW);
+    for (int s = 0; s < kDecStages; ++s) {
+      sm100::mbar_init(&full[s], 1);
+      sm100::mbar_init(&empty[s], 1);
+    }
+    sm100::mbar_init(&tfull, 1);
+    sm100::mbar_init(&mbar_max, 1);
+    sm100::mbar_init(&mbar_part, 1);
+    sm100::fence_mbar_init();
+  }
+  if (warp == 1) sm100::tmem_alloc(&tmem_holder, C::kTmemCols);
+  // X operand region of this CTA's stages: padding token rows stay zero
+  for (int i = threadIdx.x; i < nst * kDecXStage / 16; i += kDecThreads)
+    reinterpret_cast<uint4*>(smem + C::kOffX)[i] = make_uint4(0, 0, 0, 0);
+  for (int i = threadIdx.x; i < nst * C::kSfStage / 16; i += kDecThreads)
+    reinterpret_cast<uint4*>(smem + C::kOffXsf)[i] = make_uint4(0, 0, 0, 0);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem_base = tmem_holder;
+  const int Mp = (g.M + 3) & ~3;                        // tokens padded to whole 16-B vectors
+  const int rows_own = 128 / g.splits;                  // output rows this CTA reduces
+  if (threadIdx.x == 0) {   // what the peers will push: S slice maxima, S partial row blocks
+    if (FMT == MRFP4_FMT_NVFP4) sm100::mbar_arrive_expect_tx(&mbar_max, 4u * (uint32_t)g.splits);
+    sm100::mbar_arrive_expect_tx(&mbar_part, (uint32_t)(g.splits * rows_own * Mp * 4));
+  }
+
+  auto load_stage = [&](int j) {   // weight codes + SF atoms of slice stage j into ring slot j % S
+    const int slot = j % kDecStages, kb = kb0 + j;
+    sm100::mbar_arrive_expect_tx(&full[slot], kDecStageCodes + C::kSfStage);
+    sm100::tma_load_2d(smem + C::kOffW + slot * kDecStageCodes, &tmW, &full[slot], kb * 128, tile * 128);
+    sm100::bulk_load(smem + C::kOffWsf + slot * C::kSfStage,
+                     g.w_sf + ((int64_t)tile * g.sf_col_blocks + (int64_t)kb * C::kAtoms) * 512, C::kSfStage,
+                     &full[slot]);
+  };
+  // 1. the weight stream starts before anything else (independent of the predecessor kernel);
+  // two stages now, the rest right after this CTA's activation loads are in flight (the X loads
+  // are on the critical path and must not queue behind the whole weight prefetch).
+  constexpr int kEarly = 2;
+  if (warp == 0 && lane == 0)
+    for (int j = 0; j < min(nst, kEarly); ++j) load_stage(j);
+  // cluster barrier, split: every CTA's mbarriers exist before any remote store targets them
+  // (their init is released at cluster scope by fence.mbarrier_init, so the arrive is relaxed:
+  // no GPU membar); the wait sits right before the first remote store, latency hidden by the
+  // activation loads
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+  pdl_wait();
+  pdl_trigger();
+  stamp(1);
+
+  // 2. rotate this CTA's K-slice of every token (kept in registers: <= kDecSegs segments per
+  // thread, all loads of a thread in flight at once); NVFP4: the slice's max |y|, then the
+  // cluster's (= the whole tensor's) over DSMEM.  3. the slice -> SMEM operand (128-B swizzled
+  // K-major) + SF atoms.
+  //
+  // Both run twice over the same instructions: pass 0 on dummy data (all ones, fixed encode
+  // constants) while the activation loads are in flight, pass 1 on the activations.  After an
+  // L2 flush the kernel's code comes from HBM line by line as it first executes; pass 0 takes
+  // those misses under the load latency instead of on the critical path.  Pass 0 writes exactly
+  // the SMEM locations pass 1 overwrites, and its status bits are dropped.
+  const int nseg_slice = nst * 8;                 // 256 FP4 per stage = 8 segments of 32
+  uint4 v[kDecSegs][4];
+#pragma unroll
+  for (int b = 0; b < kDecSegs; ++b) {
+    const int s = threadIdx.x + b * kDecThreads;
+    const int r = s / nseg_slice, cs = s - r * nseg_slice;
+    const uint4* src = reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(g.x) + (int64_t)r * g.K +
+                                                      (int64_t)(kb0 * 256 + cs * kSeg));
+#pragma unroll
+    for (int c = 0; c < 4; ++c) v[b][c] = r < g.M ? __ldg(src + c) : make_uint4(0, 0, 0, 0);
+  }
+  if (warp == 0 && lane == 0)
+    for (int j = kEarly; j < min(nst, kDecStages); ++j) load_stage(j);
+  uint32_t bad = 0;
+  EncConsts k;                                     // pass 0: s_T = 1 (NVFP4), 4/3 (MXFP4)
+  if constexpr (FMT == MRFP4_FMT_NVFP4) {
+    k.st32 = 1.f;
+    k.st64 = 1.0;
+    k.kenc = (float)(g.qp.c64 / 6.0);
+    k.knv = (float)g.qp.c64;
+  } else {
+    k.st32 = g.qp.mx_ts;
+  }
+#ifndef MRFP4_DEC_WARM
+#define MRFP4_DEC_WARM 0   // measured: the dummy pass costs more than the code misses it hides
+#endif
+#pragma unroll 1
+  for (int pass = 1 - MRFP4_DEC_WARM; pass < 2; ++pass) {
+    u64 P[kDecSegs][kPairs];
+    if (pass) {
+#pragma unroll
+      for (int b = 0; b < kDecSegs; ++b)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const uint32_t w[4] = {v[b][c].x, v[b][c].y, v[b][c].z, v[b][c].w};
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            if constexpr (IN == MRFP4_DT_BF16) {
+              P[b][4 * c + t] = pk(__uint_as_float(w[t] << 16), __uint_as_float(w[t] & 0xFFFF0000u));
+            } else {
+              const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[t]));
+              P[b][4 * c + t] = pk(f.x, f.y);
+            }
+          }
+        }
+    } else {
+#pragma unroll
+      for (int b = 0; b < kDecSegs; ++b)
+#pragma unroll
+        for (int i = 0; i < kPairs; ++i) P[b][i] = pk(1.f, 1.f);
+    }
+    if constexpr (HK > 0) {
+#pragma unroll
+      for (int b = 0; b < kDecSegs; ++b) fwht<HK>(P[b], 0, g.qp.pm);
+    }
+    if (pass) {
+      stamp(6);
+      asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+      stamp(8);
+      if constexpr (FMT == MRFP4_FMT_NVFP4) {
+        float m = 0.f;
+#pragma unroll
+        for (int b = 0; b < kDecSegs; ++b) {   // rows >= M were zero-filled: |0| adds nothing
+          float a0, a1;
+          half_amax(P[b], a0, a1);
+          m = max3n(a0, a1, m);
+        }
+        uint32_t mb = __float_as_uint(m);
+        mb = mb > 0x7f800000u ? 0x7fc00000u : mb;
+        mb = __reduce_max_sync(0xffffffffu, mb);
+        if (lane == 0) wmax[warp] = mb;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          uint32_t x = 0;
+          for (int i = 0; i < kDecThreads / 32; ++i) x = max(x, wmax[i]);
+          for (int rr = 0; rr < g.splits; ++rr) st_async_u32(&cmaxs[split], x, &mbar_max, (uint32_t)rr);
+        }
+        stamp(7);
+        if (threadIdx.x < 4) {   // 4 lanes: s_T each, then one fp64 constant apiece (shorter chain)
+          sm100::mbar_wait(&mbar_max, 0);            // every slice's maximum has landed here
+          stamp(12);
+          uint32_t x = 0;
+          for (int rr = 0; rr < g.splits; ++rr) x = max(x, cmaxs[rr]);
+          const double top = (double)__uint_as_float(x) * g.qp.c64 / 6.0;   // quantizers.py:198-200
+          const float st32 = top > 0.0 ? __double2float_rn(top / 448.0) : 1.0f;
+          nv_consts_st_part(g.qp, g.c6, st32, (int)threadIdx.x, sk);
+          stamp(13);
+        }
+        __syncthreads();
+        k = sk;
+      }
+      stamp(2);
+    }
+
+    uint32_t bq = 0;
+#pragma unroll
+    for (int b = 0; b < kDecSegs; ++b) {
+      const int s = threadIdx.x + b * kDecThreads;
+      const int r = s / nseg_slice, cs = s - r * nseg_slice;     // token row, segment in the slice
+      if (r >= g.M) continue;
+      const int j = cs >> 3, chunk = cs & 7;                     // stage, 16-B chunk in the 128-B row
+      float a0, a1;
+      half_amax(P[b], a0, a1);
+      GroupScale s0, s1;
+      uint32_t sfc;
+      if constexpr (FMT == MRFP4_FMT_NVFP4) {
+        s0 = nv_group_scale(a0, g.qp, k.kenc, k.knv, k.st32, k.st64, k.zero_code);
+        s1 = nv_group_scale(a1, g.qp, k.kenc, k.knv, k.st32, k.st64, k.zero_code);
+        if (__float_as_uint(a0) >= 0x7f800000u || __float_as_uint(a1) >= 0x7f800000u) bq |= MRFP4_STATUS_NONFINITE;
+        if (s0.code == 0 || s1.code == 0) bq |= MRFP4_STATUS_SCALE_UNDERFLOW;
+        sfc = s0.code | (s1.code << 8);
+      } else {
+        const float a = max3n(a0, a1, 0.f);
+        if (__float_as_uint(a) >= 0x7f800000u) bq |= MRFP4_STATUS_NONFINITE;
+        s0 = mx_group_scale(a, g.qp);
+        s1 = s0;
+        sfc = s0.code;
+      }
+      uint32_t w4[4];
+      quantize_seg<true>(P[b], s0, s1, k.st32, g.qp, w4);
+      *reinterpret_cast<uint4*>(smem + C::kOffX + j * kDecXStage + r * 128 + ((chunk ^ (r & 7)) << 4)) =
+          make_uint4(w4[0], w4[1], w4[2], w4[3]);
+      // SF column of this segment within the stage: NVFP4 2 * chunk (+1), MXFP4 chunk
+      uint8_t* sfst = smem + C::kOffXsf + j * C::kSfStage;
+      const int col = FMT == MRFP4_FMT_NVFP4 ? 2 * chunk : chunk;
+      const int off = (col >> 2) * 512 + (r & 31) * 16 + ((r >> 5) & 3) * 4 + (col & 3);
+      if constexpr (FMT == MRFP4_FMT_NVFP4)
+        *reinterpret_cast<uint16_t*>(sfst + off) = (uint16_t)sfc;
+      else
+        sfst[off] = (uint8_t)sfc;
+    }
+    if (pass) bad = bq;
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic SMEM writes -> tcgen05 reads
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  stamp(3);
+
+  // 4. MMAs (warp 1) and the rest of the weight stream (warp 0)
+  if (warp == 0) {
+    if (lane == 0)
+      for (int j = kDecStages; j < nst; ++j) {
+        sm100::mbar_wait(&empty[j % kDecStages], ((j / kDecStages) & 1) ^ 1);
+        load_stage(j);
+      }
+  } else if (warp == 1) {
+    const uint32_t el = sm100::elect_lane();
+    const uint32_t idesc = sm100::idesc_fp4(128, g.NT, VEC == 32, 0, 0);
+    const uint64_t wdesc0 = sm100::smem_desc(sm100::smem_u32(smem + C::kOffW), 16, 1024, 2);
+    const uint64_t xdesc0 = sm100::smem_desc(sm100::smem_u32(smem + C::kOffX), 16, 1024, 2);
+    for (int j = 0; j < nst; ++j) {
+      const int slot = j % kDecStages;
+      sm100::mbar_wait(&full[slot], (j / kDecStages) & 1);
+      sm100::tc_fence_after();
+      const uint32_t sfa = tmem_base + 32 + slot * C::kSfCols, sfb = sfa + C::kAtoms * 4;
+      const uint32_t wsf = sm100::smem_u32(smem + C::kOffWsf + slot * C::kSfStage);
+      const uint32_t xsf = sm100::smem_u32(smem + C::kOffXsf + j * C::kSfStage);
+#pragma unroll
+      for (int a = 0; a < C::kAtoms; ++a) {
+        tc_cp_if(el, sfa + a * 4, sm100::smem_desc(wsf + a * 512, 0, 128, 0));
+        tc_cp_if(el, sfb + a * 4, sm100::smem_desc(xsf + a * 512, 0, 128, 0));
+      }
+      const uint64_t wd = dadd(wdesc0, (uint32_t)(slot * (kDecStageCodes >> 4)));
+      const uint64_t xd = dadd(xdesc0, (uint32_t)(j * (kDecXStage >> 4)));
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const uint32_t atom = VEC == 16 ? kk : (kk >> 1);
+        const uint32_t sfid = VEC == 16 ? 0u : (uint32_t)(kk & 1) * 2u;
+        const uint32_t id = idesc | (sfid << 4) | (sfid << 29);
+        tc_mma_fp4_if(el, VEC, tmem_base, dadd(wd, 2 * kk), dadd(xd, 2 * kk), id, (sfa + atom * 4) | (sfid << 30),
+                      (sfb + atom * 4) | (sfid << 30), (j | kk) ? 1u : 0u);
+      }
+      tc_commit_if(&empty[slot], el);
+      __syncwarp();
+    }
+    tc_commit_if(&tfull, el);
+    __syncwarp();
+  }
+
+  // 5. epilogue: warps 4-7 read the fp32 partial D^T (one weight row per thread) from TMEM and
+  // push it to the CTA of the cluster that reduces that row ([src rank][row][token] in its SMEM,
+  // st.async counted on its mbar_part); each CTA then sums its rows over the S sources in rank
+  // order (deterministic) and stores Y.
+  float* recv = reinterpret_cast<float*>(smem + C::kOffPart);
+  if (warp >= 4 && warp < 8) {
+    const int q = warp & 3;
+    sm100::mbar_wait(&tfull, 0);
+    if (warp == 4 && lane == 0 && g.trace) g.trace[blockIdx.x * 16 + 4] = globaltimer();
+    sm100::tc_fence_after();
+    uint32_t r[32];
+    sm100::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16), r);
+    sm100::tmem_ld_wait();
+    if (warp == 4 && lane == 0 && g.trace) g.trace[blockIdx.x * 16 + 9] = globaltimer();
+    const int nl = q * 32 + lane, owner = nl / rows_own, nloc = nl - owner * rows_own;
+    const uint32_t dst = mapa_u32(recv + ((split * rows_own + nloc) * Mp), (uint32_t)owner);
+    const uint32_t bar = mapa_u32(&mbar_part, (uint32_t)owner);
+#pragma unroll
+    for (int m4 = 0; m4 < 32; m4 += 4)
+      if (m4 < Mp) st_async_v4(dst + 4 * m4, r[m4], r[m4 + 1], r[m4 + 2], r[m4 + 3], bar);
+    if (warp == 4 && lane == 0 && g.trace) g.trace[blockIdx.x * 16 + 10] = globaltimer();
+  }
+  sm100::mbar_wait(&mbar_part, 0);               // all S partials of this CTA's rows have landed
+  if (warp == 4 && lane == 0 && g.trace) g.trace[blockIdx.x * 16 + 11] = globaltimer();
+  {
+    // rolled loops: this code runs once per launch, and after an L2 flush every instruction of
+    // it is fetched from HBM on the critical path -- fewer is faster
+    const float alpha = k.st32 * __ldg(g.w_ts);
+#pragma unroll 1
+    for (int e = threadIdx.x; e < g.M * rows_own; e += kDecThreads) {
+      const int m = e / rows_own, nloc = e - m * rows_own;
+      float acc = -0.f;
+#pragma unroll 1
+      for (int sp = 0; sp < g.splits; ++sp) acc += recv[(sp * rows_own + nloc) * Mp + m];
+      const int64_t n = (int64_t)tile * 128 + split * rows_own + nloc;
+      const float v = acc * alpha;
+      if (g.out_f32) static_cast<float*>(g.d)[(int64_t)m * g.ldd + n] = v;
+      else static_cast<__nv_bfloat16*>(g.d)[(int64_t)m * g.ldd + n] = __float2bfloat16_rn(v);
+    }
+  }
+  if (bad && g.status) atomicOr(g.status, bad);
+  if (warp == 4 && lane == 0 && g.trace) g.trace[blockIdx.x * 16 + 5] = globaltimer();
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc(tmem_base, C::kTmemCols);
+  }
+}
+
+}  // namespace
+
+// Cluster plan of the fused decode linear: splits (= cluster size, a power of 2 <= 8) large
+// enough that every thread holds at most 2 segments of the slice (M * stages <= 64), and, within
+// that, about one CTA per SM.  Returns false when no such plan exists.
+bool decode_plan(int64_t M, int64_t N, int64_t K, int* splits, int* kb_per) {
+  const int row_tiles = (int)ceil_div(N, 128), num_kb = (int)(K / 256);
+  int sp = 1;
+  while (sp < kDecMaxSplits && (int64_t)ceil_div(num_kb, sp) * M * 8 > kDecSegsPerCta) sp *= 2;
+  while (sp < kDecMaxSplits && row_tiles * sp * 2 <= device_sms() && sp * 2 <= num_kb) sp *= 2;
+  const int per = (int)ceil_div(num_kb, sp);
+  *splits = sp;
+  *kb_per = per;
+  return (int64_t)per * M * 8 <= kDecSegsPerCta && per <= kDecMaxSliceStages && sp <= num_kb &&
+         (int64_t)(sp - 1) * per < num_kb && row_tiles * sp <= device_sms();   // one wave
+}
+
+size_t decode_workspace_bytes(int64_t, int64_t, int64_t) { return 0; }
+
+// Returns MRFP4_EUNSUPPORTED when the shape is not a decode shape (the caller uses K1 + K2).
+int launch_linear_decode(const void* x, int x_dtype, int64_t M, int64_t K, int fmt, int hk, const uint8_t* w,
+                         const uint8_t* w_sf, const float* w_ts, int64_t N, void* d, int d_dtype, int64_t ldd,
+                         void* ws, size_t ws_bytes, uint32_t* status, cudaStream_t s) {
+  if (M < 1 || M > 32 || K % 256 || K < 256 || N % 128 || (hk != 0 && hk != 16 && hk != 32) ||
+      (x_dtype != MRFP4_DT_BF16 && x_dtype != MRFP4_DT_F16) || M * K > (1 << 18))
+    return MRFP4_EUNSUPPORTED;
+
+  DecArgs g{};
+  g.x = x;
+  g.M = (int)M;
+  g.K = (int)K;
+  g.N = (int)N;
+  g.NT = M <= 16 ? 16 : 32;
+  g.ldd = ldd;
+  g.fmt = fmt;
+  g.hk = hk;
+  g.w_sf = w_sf;
+  g.w_ts = w_ts;
+  g.d = d;
+  g.out_f32 = d_dtype == MRFP4_DT_F32;
+  g.status = status;
+  g.trace = g_dec_trace;
+  const int G = fmt == MRFP4_FMT_MXFP4 ? 32 : 16;
+  g.sf_col_blocks = ceil_div(K / G, 4);
+  g.row_tiles = (int)(N / 128);
+  g.num_kb = (int)(K / 256);
+  if (!decode_plan(M, N, K, &g.splits, &g.kb_per)) return MRFP4_EUNSUPPORTED;
+  (void)ws;
+  (void)ws_bytes;
+  g.qp.c64 = hk ? 1.0 / std::sqrt((double)hk) : 1.0;
+  g.qp.kraw = (float)(g.qp.c64 / 6.0);
+  g.c6 = g.qp.c64 / 6.0;
+  g.qp.mx_ts = 1.33333337306976318359375f;
+  g.qp.kmx = (float)(g.qp.c64 / (double)g.qp.mx_ts);
+  const float pm[2] = {1.f, -1.f};
+  memcpy(&g.qp.pm, pm, sizeof(pm));
+
+  auto encode = tensor_map_encoder();
+  if (!encode) return MRFP4_ECUDA;
+  CUtensorMap tm;
+  cuuint64_t dims[2] = {(cuuint64_t)(K / 2), (cuuint64_t)N};
+  cuuint64_t strides[1] = {(cuuint64_t)(K / 2)};
+  cuuint32_t box[2] = {128, 128};
+  cuuint32_t estr[2] = {1, 1};
+  if (encode(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(w), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return MRFP4_ECUDA;
+  auto go = [&](auto kern, int smem) -> int {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+      return MRFP4_ECUDA;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(g.row_tiles * g.splits);
+    cfg.blockDim = dim3(kDecThreads);
+    cfg.dynamicSmemBytes = (size_t)smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;     // one cluster per weight row tile
+    attr[0].val.clusterDim.x = (unsigned)g.splits;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
+    return cudaLaunchKernelEx(&cfg, kern, tm, g) == cudaSuccess ? MRFP4_OK : MRFP4_ECUDA;
+  };
+#define MRFP4_DEC(IN, V, H) \
+  if (x_dtype == IN && G == V && hk == H) return go(k_linear_decode<IN, V, H>, DecCfg<V>::kSmem);
+  MRFP4_DEC(MRFP4_DT_BF16, 16, 16) MRFP4_DEC(MRFP4_DT_BF16, 16, 32) MRFP4_DEC(MRFP4_DT_BF16, 16, 0)
+  MRFP4_DEC(MRFP4_DT_BF16, 32, 16) MRFP4_DEC(MRFP4_DT_BF16, 32, 32) MRFP4_DEC(MRFP4_DT_BF16, 32, 0)
+  MRFP4_DEC(MRFP4_DT_F16, 16, 16) MRFP4_DEC(MRFP4_DT_F16, 16, 32) MRFP4_DEC(MRFP4_DT_F16, 16, 0)
+  MRFP4_DEC(MRFP4_DT_F16, 32, 16) MRFP4_DEC(MRFP4_DT_F16, 32, 32) MRFP4_DEC(MRFP4_DT_F16, 32, 0)
+#undef MRFP4_DEC
+  return MRFP4_EUNSUPPORTED;
+}
+
+}  // namespace mrfp4
+
+extern "C" void mrfp4_debug_decode_trace(unsigned long long* buf) { mrfp4::g_dec_trace = buf; }
+
+// perf experiments: one thread writes %globaltimer to *dst (brackets a launch in the trace)
+namespace {
+__global__ void k_stamp(unsigned long long* dst) { *dst = mrfp4::globaltimer(); }
+}  // namespace
+extern "C" void mrfp4_debug_stamp(unsigned long long* dst, void* stream) {
+  k_stamp<<<1, 1, 0, (cudaStream_t)stream>>>(dst);
+}

@@ -210,6 +210,15 @@ __device__ __forceinline__ uint32_t cvt_e2m1x8(const float (&u)[8]) {
   return r;
 }
 
+// One float -> its E2M1 code (satfinite, RNE) in the low nibble.
+__device__ __forceinline__ uint32_t cvt_e2m1x1(float x) {
+  uint16_t r;
+  asm("{\n\t.reg .b8 b0;\n\tcvt.rn.satfinite.e2m1x2.f32 b0, %1, %2;\n\tcvt.u16.u8 %0, b0;\n\t}"
+      : "=h"(r)
+      : "f"(0.0f), "f"(x));
+  return r;
+}
+
 // A nibble whose magnitude rounded to 0 must be 0x0, not 0x8 (formats.py:110).
 __device__ __forceinline__ uint32_t fix_neg_zero(uint32_t w) {
   const uint32_t mag = w & 0x77777777u;
@@ -295,8 +304,67 @@ __device__ __forceinline__ EncConsts nv_consts_st(const AQParams& p, float st32)
   return k;
 }
 
+// nv_consts_st split over 4 threads (part 0..3 each writes its own field of `k`).
+// c6 = RN64(c64 / 6), precomputed (the same double numpy forms first in c64 / 6 / s_T).
+__device__ __forceinline__ void nv_consts_st_part(const AQParams& p, double c6, float st32, int part, EncConsts& k) {
+  const double st64 = (double)st32;
+  if (part == 0) {
+    k.st32 = st32;
+    k.st64 = st64;
+  } else if (part == 1) {
+    k.zero_code = e4m3_rne64(1.0 / st64);
+  } else if (part == 2) {
+    k.kenc = __double2float_rn(c6 / st64);
+  } else {
+    k.knv = __double2float_rn(p.c64 / st64);
+  }
+}
+
+struct SegVals { u64 p[kPairs]; };
+struct Words4 { uint32_t w[4]; };
+
+// The rare exact path of quantize_seg, out of line (passed by value: the caller's registers stay
+// registers) so that the hot instruction stream stays dense: every element whose code could
+// depend on the last bits of its fp32 value is re-decided in float64.  Rolled over the 4 words,
+// 8 independent elements per iteration.
+__device__ __noinline__ Words4 requant_exact(SegVals v, GroupScale s0, GroupScale s1, float ts, double c64,
+                                             Words4 w) {
+  constexpr float kEps = 3.814697265625e-06f;  // 2^-18
+#pragma unroll 1
+  for (int wi = 0; wi < 4; ++wi) {
+    const bool lo = wi < 2;
+    const float gf = lo ? s0.f : s1.f, gdec = lo ? s0.dec : s1.dec;
+    const bool slow = lo ? s0.slow_all : s1.slow_all;
+    u64 q[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      q[t] = v.p[t];
+#pragma unroll
+      for (int z = 1; z < 4; ++z) q[t] = wi == z ? v.p[4 * z + t] : q[t];
+    }
+    uint32_t word = w.w[0];
+#pragma unroll
+    for (int z = 1; z < 4; ++z) word = wi == z ? w.w[z] : word;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const float x = (t & 1) ? hi_of(q[t / 2]) : lo_of(q[t / 2]);
+      if (slow || ((cvt_e2m1x1(x * (gf * (1.f + kEps))) ^ cvt_e2m1x1(x * (gf * (1.f - kEps)))) & 0xFu)) {
+        const uint32_t c = fp4_code_exact(x, c64, ts, gdec);
+        word = (word & ~(0xFu << (4 * t))) | (c << (4 * t));
+      }
+    }
+#pragma unroll
+    for (int z = 0; z < 4; ++z)
+      if (wi == z) w.w[z] = word;
+  }
+  return w;
+}
+
 // Codes of the segment as 4 words (word w = elements 8w..8w+7 = pairs 4w..4w+3).
 // s0 scales pairs 0..7 (elements 0..15), s1 pairs 8..15.
+// kOutOfLine: the rare exact path as a call (requant_exact) instead of inline code -- for
+// once-per-launch code (the decode kernel), where every inline instruction is fetched cold.
+template <bool kOutOfLine = false>
 __device__ __forceinline__ void quantize_seg(const u64 (&P)[kPairs], const GroupScale& s0, const GroupScale& s1,
                                              float ts, const AQParams& p, uint32_t (&w)[4]) {
   constexpr float kEps = 3.814697265625e-06f;  // 2^-18
@@ -317,7 +385,15 @@ __device__ __forceinline__ void quantize_seg(const u64 (&P)[kPairs], const Group
     w[wi] = a;
     diff |= a ^ b;
   }
-  if (diff | (uint32_t)(s0.slow_all | s1.slow_all)) {
+  if (kOutOfLine && (diff | (uint32_t)(s0.slow_all | s1.slow_all))) {
+    SegVals sv;
+#pragma unroll
+    for (int i = 0; i < kPairs; ++i) sv.p[i] = P[i];
+    const Words4 r = requant_exact(sv, s0, s1, ts, p.c64, Words4{{w[0], w[1], w[2], w[3]}});
+#pragma unroll
+    for (int wi = 0; wi < 4; ++wi) w[wi] = r.w[wi];
+  }
+  if (!kOutOfLine && (diff | (uint32_t)(s0.slow_all | s1.slow_all))) {
 #pragma unroll
     for (int wi = 0; wi < 4; ++wi) {
       const GroupScale& g = wi < 2 ? s0 : s1;

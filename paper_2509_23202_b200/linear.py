@@ -196,6 +196,36 @@ def _gemm_launch(L, a, w, out, ws, nbytes, stream):
         _lib.ptr(ws), nbytes, stream))
 
 
+_DECODE = os.environ.get("MRFP4_DECODE", "1") != "0"   # A/B switch for the fused decode kernel
+_IN = {torch.bfloat16: _lib.DT_BF16, torch.float16: _lib.DT_F16}
+
+
+def decode_eligible(M: int, w: PackedWeight, x_dtype) -> bool:
+    """Shapes the one-kernel decode linear (mrfp4_linear_decode) takes."""
+    if not (_DECODE and 1 <= M <= 32 and w.K % 256 == 0 and w.N % 128 == 0 and w.had_k in (0, 16, 32)
+            and M * w.K <= (1 << 18) and x_dtype in _IN):
+        return False
+    return int(_lib.lib().mrfp4_linear_decode_ctas(M, w.N, w.K)) > 0
+
+
+def decode_workspace_bytes(M: int, w: PackedWeight) -> int:
+    return int(_lib.lib().mrfp4_linear_decode_workspace(M, w.N, w.K))
+
+
+def _linear_decode(x2: torch.Tensor, w: PackedWeight, out: torch.Tensor, ws, status) -> None:
+    """K1 + K2 of a decode-sized linear in one launch (see include/mrfp4.h)."""
+    M, K = x2.shape
+    nbytes = decode_workspace_bytes(M, w)
+    with torch.cuda.device(out.device):
+        stream = _lib.stream_ptr(torch, out.device)
+        if ws is None:
+            ws = _gemm_workspace(out.device, ("dec", stream), nbytes)
+        _lib.check(_lib.lib().mrfp4_linear_decode(
+            _lib.ptr(x2), _IN[x2.dtype], M, K, w.fmt, w.had_k, _lib.ptr(w.codes), _lib.ptr(w.sf),
+            _lib.ptr(w.tensor_scale_dev), w.N, _lib.ptr(out), _OUT[out.dtype], out.stride(0), _lib.ptr(ws), nbytes,
+            _lib.ptr(status), stream))
+
+
 def quantized_linear(x, w: PackedWeight, *, out_dtype=torch.bfloat16, out: torch.Tensor | None = None,
                      check: bool = False) -> torch.Tensor:
     """y = Q(x H_k) Q(W H_k)^T for x [..., K] (bf16/fp16/fp32), W prepared by prepare_weight."""
@@ -208,6 +238,15 @@ def quantized_linear(x, w: PackedWeight, *, out_dtype=torch.bfloat16, out: torch
     M, K = x2.shape
     if K != w.K:
         raise DataError(f"activation K={K} does not match weight K={w.K}")
+    if decode_eligible(M, w, x2.dtype) and x2.is_contiguous():
+        if out is None:
+            out = torch.empty((M, w.N), dtype=out_dtype, device=x2.device)
+        _check_out(out, M, w)
+        status = torch.zeros(1, dtype=torch.int32, device=x2.device) if check else None
+        _linear_decode(x2, w, out, None, status)
+        if check and int(status.item()) & (_lib.STATUS_NONFINITE | _lib.STATUS_SCALE_UNDERFLOW):
+            raise DataError("non-finite element")
+        return out.reshape(*lead, w.N) if lead is not None and len(lead) != 1 else out
     # check=False never reads the status word: reuse the stream's scratch (no zero-fill launch)
     a = alloc_result(M, K, w.fmt, w.had_k, x2.device, None if check else stream_scratch(x2.device))
     act_quant_into(x2, w.fmt, w.had_k, a.codes, a.sf, a.tensor_scale_dev, a.scratch)
@@ -378,7 +417,8 @@ class GraphedLinear:
         self.a = alloc_result(M, w.K, w.fmt, w.had_k, dev)
         # The graph captures raw pointers: it owns its split-K workspace (zeroed once; every
         # replay leaves the counters zero again) instead of borrowing the shared eager one.
-        nbytes = gemm_workspace_bytes(M, w)
+        self.decode = decode_eligible(M, w, x_dtype)
+        nbytes = decode_workspace_bytes(M, w) if self.decode else gemm_workspace_bytes(M, w)
         self.ws = torch.zeros(max(nbytes, 1), dtype=torch.uint8, device=dev)
         side = torch.cuda.Stream(dev)
         side.wait_stream(torch.cuda.current_stream(dev))
@@ -393,6 +433,9 @@ class GraphedLinear:
         torch.cuda.synchronize(dev)
 
     def _run(self):
+        if self.decode:
+            _linear_decode(self.x, self.w, self.y, self.ws, None)
+            return
         act_quant_into(self.x, self.w.fmt, self.w.had_k, self.a.codes, self.a.sf, self.a.tensor_scale_dev,
                        self.a.scratch)
         gemm(self.a, self.w, self.y, ws=self.ws)
