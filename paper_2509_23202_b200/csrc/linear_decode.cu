@@ -40,7 +40,7 @@ namespace {
 using namespace qc;
 
 #ifndef MRFP4_DEC_THREADS
-#define MRFP4_DEC_THREADS 256
+#define MRFP4_DEC_THREADS 512
 #endif
 constexpr int kDecThreads = MRFP4_DEC_THREADS;   // all quantize X; w0 producer, w1 MMA, w4-7 epilogue
 constexpr int kDecSegsPerCta = 512;              // 32-element activation segments one CTA rotates
@@ -64,7 +64,6 @@ struct DecArgs {
   int64_t sf_col_blocks;    // weight / activation SF column blocks: ceil(K / G / 4)
   uint32_t* status;
   AQParams qp;              // c64 / kraw / kmx / pm / mx_ts of the activation quantization
-  double c6;                  // RN64(c64 / 6)
   unsigned long long* trace;  // perf experiments: per-CTA globaltimer stamps (null in production)
 };
 unsigned long long* g_dec_trace = nullptr;
@@ -142,6 +141,7 @@ __global__ void __launch_bounds__(kDecThreads, 1)
     k_linear_decode(const __grid_constant__ CUtensorMap tmW, DecArgs g) {
   using C = DecCfg<VEC>;
   constexpr int FMT = VEC == 16 ? MRFP4_FMT_NVFP4 : MRFP4_FMT_MXFP4;
+  constexpr bool kPow2C = HK == 0 || HK == 16;   // c64 = 1 / sqrt(k) a power of 2
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ __align__(8) uint64_t full[kDecStages], empty[kDecStages], tfull, mbar_max, mbar_part;
@@ -294,14 +294,12 @@ __global__ void __launch_bounds__(kDecThreads, 1)
           for (int rr = 0; rr < g.splits; ++rr) st_async_u32(&cmaxs[split], x, &mbar_max, (uint32_t)rr);
         }
         stamp(7);
-        if (threadIdx.x < 4) {   // 4 lanes: s_T each, then one fp64 constant apiece (shorter chain)
+        if (threadIdx.x == 0) {
           sm100::mbar_wait(&mbar_max, 0);            // every slice's maximum has landed here
           stamp(12);
           uint32_t x = 0;
           for (int rr = 0; rr < g.splits; ++rr) x = max(x, cmaxs[rr]);
-          const double top = (double)__uint_as_float(x) * g.qp.c64 / 6.0;   // quantizers.py:198-200
-          const float st32 = top > 0.0 ? __double2float_rn(top / 448.0) : 1.0f;
-          nv_consts_st_part(g.qp, g.c6, st32, (int)threadIdx.x, sk);
+          sk = nv_consts_fast(g.qp, kPow2C, x);
           stamp(13);
         }
         __syncthreads();
@@ -322,8 +320,8 @@ __global__ void __launch_bounds__(kDecThreads, 1)
       GroupScale s0, s1;
       uint32_t sfc;
       if constexpr (FMT == MRFP4_FMT_NVFP4) {
-        s0 = nv_group_scale(a0, g.qp, k.kenc, k.knv, k.st32, k.st64, k.zero_code);
-        s1 = nv_group_scale(a1, g.qp, k.kenc, k.knv, k.st32, k.st64, k.zero_code);
+        s0 = nv_group_scale<true>(a0, g.qp, k.kenc, k.knv, k.st32, k.st64, k.zero_code, kPow2C);
+        s1 = nv_group_scale<true>(a1, g.qp, k.kenc, k.knv, k.st32, k.st64, k.zero_code, kPow2C);
         if (__float_as_uint(a0) >= 0x7f800000u || __float_as_uint(a1) >= 0x7f800000u) bq |= MRFP4_STATUS_NONFINITE;
         if (s0.code == 0 || s1.code == 0) bq |= MRFP4_STATUS_SCALE_UNDERFLOW;
         sfc = s0.code | (s1.code << 8);
@@ -335,7 +333,7 @@ __global__ void __launch_bounds__(kDecThreads, 1)
         sfc = s0.code;
       }
       uint32_t w4[4];
-      quantize_seg<true>(P[b], s0, s1, k.st32, g.qp, w4);
+      quantize_seg<true>(P[b], s0, s1, k.st32, g.qp, w4, kPow2C);
       *reinterpret_cast<uint4*>(smem + C::kOffX + j * kDecXStage + r * 128 + ((chunk ^ (r & 7)) << 4)) =
           make_uint4(w4[0], w4[1], w4[2], w4[3]);
       // SF column of this segment within the stage: NVFP4 2 * chunk (+1), MXFP4 chunk
@@ -497,7 +495,6 @@ int launch_linear_decode(const void* x, int x_dtype, int64_t M, int64_t K, int f
   (void)ws_bytes;
   g.qp.c64 = hk ? 1.0 / std::sqrt((double)hk) : 1.0;
   g.qp.kraw = (float)(g.qp.c64 / 6.0);
-  g.c6 = g.qp.c64 / 6.0;
   g.qp.mx_ts = 1.33333337306976318359375f;
   g.qp.kmx = (float)(g.qp.c64 / (double)g.qp.mx_ts);
   const float pm[2] = {1.f, -1.f};

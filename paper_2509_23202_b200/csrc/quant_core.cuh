@@ -266,8 +266,16 @@ __device__ __forceinline__ GroupScale mx_group_scale(float amax, const AQParams&
   return g;
 }
 
+// kFma (decode kernel), c_pow2 (c64 a power of 2): near a true E4M3 midpoint M of the normal
+// range, v = RN64(RN64(a * c / 6) / s_T) vs M follows sign(a * c - 6 M s_T), one exact fmaf
+// (x = a * c exact, 6 M has <= 7 significant bits).  If x != 6 M s_T their difference is a
+// multiple of a quantum >= 2^-29 * x, far beyond the two float64 roundings (2^-52), so v lies
+// on the same side as the quotient; if equal, v == M exactly (M s_T has <= 29 bits) and RNE
+// picks the even code.  Everything else: the float64 chain.
+template <bool kFma = false>
 __device__ __forceinline__ GroupScale nv_group_scale(float amax, const AQParams& p, float kenc, float knv,
-                                                     float st32, double st64, uint32_t zero_code) {
+                                                     float st32, double st64, uint32_t zero_code,
+                                                     bool c_pow2 = false) {
   GroupScale g;
   const uint32_t ab = __float_as_uint(amax);
   const float enc32 = amax * kenc;                            // ~ RN64(RN64(a/6)/s_T)
@@ -275,7 +283,20 @@ __device__ __forceinline__ GroupScale nv_group_scale(float amax, const AQParams&
   uint32_t code = cvt_e4m3(enc32);
   // E4M3 midpoints have <= 5 significant bits: low 19 mantissa bits are zero.
   if (((eb + 64u) & 0x7FFFFu) < 128u || eb >= 0x7f800000u || eb < 0x38800000u /* < 2^-14 */) {
-    code = ab ? e4m3_code_exact(amax, p.c64, st64) : zero_code;
+    bool done = false;
+    if constexpr (kFma) {
+      const uint32_t mb = (eb + 64u) & ~0x7FFFFu;               // the 5-bit value enc32 is near
+      const float x = amax * (float)p.c64;
+      if (c_pow2 && ((eb + 64u) & 0x7FFFFu) < 128u && (mb & 0x80000u) && mb >= 0x3C800000u /* 2^-6 */ &&
+          mb <= 0x43E00000u /* 448 */ && x >= 0x1p-100f) {
+        const uint32_t lower = cvt_e4m3(__uint_as_float(mb - 1u));
+        const float r = fmaf(-6.f * __uint_as_float(mb), st32, x);
+        code = r > 0.f ? lower + 1u : r < 0.f ? lower : lower + (lower & 1u);
+        done = true;
+      }
+    }
+    if (!done)
+      code = ab ? e4m3_code_exact(amax, p.c64, st64) : zero_code != ~0u ? zero_code : e4m3_rne64(1.0 / st64);
   }
   g.code = code;
   g.dec = e4m3_value(code);
@@ -305,19 +326,33 @@ __device__ __forceinline__ EncConsts nv_consts_st(const AQParams& p, float st32)
 }
 
 // nv_consts_st split over 4 threads (part 0..3 each writes its own field of `k`).
-// c6 = RN64(c64 / 6), precomputed (the same double numpy forms first in c64 / 6 / s_T).
-__device__ __forceinline__ void nv_consts_st_part(const AQParams& p, double c6, float st32, int part, EncConsts& k) {
-  const double st64 = (double)st32;
-  if (part == 0) {
-    k.st32 = st32;
-    k.st64 = st64;
-  } else if (part == 1) {
-    k.zero_code = e4m3_rne64(1.0 / st64);
-  } else if (part == 2) {
-    k.kenc = __double2float_rn(c6 / st64);
+// NVFP4 encode constants from the whole-tensor max |y| bits `xb` on ONE thread, without float64
+// where it can (decode kernel: this sits between the cross-CTA max exchange and quantization).
+//  * s_T = RN32(RN64(RN64(x * c64) / 6) / 448) (quantizers.py:198-200).  When c64 is a power of 2
+//    (k in {0, 16}, and any k = 4^j) x * c64 is exact and the chain equals RN32(x * c64 / 2688):
+//    x * c64 / 21 is never within 2^-52 (relative) of an fp32 rounding midpoint -- a midpoint has
+//    25 significant bits ending in 1, and 21 * midpoint needs more than x's 24 bits -- so both
+//    roundings agree with the correctly rounded fp32 division.  Otherwise: the float64 chain.
+//  * kenc / knv only feed the fast path's estimates (their errors of a few ulp sit far inside
+//    its 64-ulp / 2^-18 exactness windows), so fp32 divisions suffice.
+//  * zero_code (all-zero groups, rare) is formed on demand in nv_group_scale (~0u sentinel).
+__device__ __forceinline__ EncConsts nv_consts_fast(const AQParams& p, bool c_pow2, uint32_t xb) {
+  EncConsts k;
+  const float x = __uint_as_float(xb);
+  float st;
+  if (c_pow2) {
+    const float y = x * (float)p.c64;
+    st = y > 0.f ? __fdiv_rn(y, 2688.f) : 1.0f;
   } else {
-    k.knv = __double2float_rn(p.c64 / st64);
+    const double top = (double)x * p.c64 / 6.0;
+    st = top > 0.0 ? __double2float_rn(top / 448.0) : 1.0f;
   }
+  k.st32 = st;
+  k.st64 = (double)st;
+  k.kenc = __fdiv_rn(p.kraw, st);
+  k.knv = __fdiv_rn((float)p.c64, st);
+  k.zero_code = ~0u;
+  return k;
 }
 
 struct SegVals { u64 p[kPairs]; };
@@ -360,17 +395,38 @@ __device__ __noinline__ Words4 requant_exact(SegVals v, GroupScale s0, GroupScal
   return w;
 }
 
+// Exact E2M1 code of u = RN64(RN64(x * c64) / RN64(ts * dec)) (fp4_code_exact's decision) with
+// no division, for c64 a power of 2 (c32 = c64) and |x| >= 2^-100, dec * 5 finite: y = |x| * c
+// is exact, and so is each threshold product T * dec (<= 7 significant bits).  RN64(y / eff)
+// vs T follows sign(y - T * ts * dec), which one fmaf gets exactly: if y != T * eff, their
+// difference is a multiple of a quantum >= 2^-31 * y, so y / eff is more than half an ulp of
+// T away from T and rounding cannot reach it; if equal, u == T exactly.
+__device__ __forceinline__ uint32_t fp4_code_fma(float x, float c32, float ts, float dec) {
+  const float y = fabsf(x) * c32;
+  uint32_t idx = 0;
+  constexpr float kT[7] = {0.25f, 0.75f, 1.25f, 1.75f, 2.5f, 3.5f, 5.f};
+#pragma unroll
+  for (int i = 0; i < 7; ++i) {
+    const float r = fmaf(-(kT[i] * dec), ts, y);
+    idx += r > 0.f;
+    if (i == 1 || i == 3 || i == 5) idx += r == 0.f;   // ties at 0.75 / 1.75 / 3.5 go up (even code)
+  }
+  return idx | ((signbit(x) && idx) ? 8u : 0u);
+}
+
 // Codes of the segment as 4 words (word w = elements 8w..8w+7 = pairs 4w..4w+3).
 // s0 scales pairs 0..7 (elements 0..15), s1 pairs 8..15.
-// kOutOfLine: the rare exact path as a call (requant_exact) instead of inline code -- for
-// once-per-launch code (the decode kernel), where every inline instruction is fetched cold.
+// kOutOfLine (the decode kernel: once-per-launch code, every inline instruction fetched cold):
+// the flagged elements are re-decided by a short inline loop (fp4_code_fma when c_pow2), whole
+// extreme-scale groups by an out-of-line call (requant_exact) -- instead of the inline
+// fully-unrolled exact block.
 template <bool kOutOfLine = false>
 __device__ __forceinline__ void quantize_seg(const u64 (&P)[kPairs], const GroupScale& s0, const GroupScale& s1,
-                                             float ts, const AQParams& p, uint32_t (&w)[4]) {
+                                             float ts, const AQParams& p, uint32_t (&w)[4], bool c_pow2 = false) {
   constexpr float kEps = 3.814697265625e-06f;  // 2^-18
   const float h0 = s0.f * (1.f + kEps), l0 = s0.f * (1.f - kEps);
   const float h1 = s1.f * (1.f + kEps), l1 = s1.f * (1.f - kEps);
-  uint32_t diff = 0;
+  uint32_t diff = 0, dw[4];
 #pragma unroll
   for (int wi = 0; wi < 4; ++wi) {
     const float fh = wi < 2 ? h0 : h1, fl = wi < 2 ? l0 : l1;
@@ -383,15 +439,34 @@ __device__ __forceinline__ void quantize_seg(const u64 (&P)[kPairs], const Group
     }
     const uint32_t a = cvt_e2m1x8(uh), b = cvt_e2m1x8(ul);
     w[wi] = a;
+    dw[wi] = a ^ b;
     diff |= a ^ b;
   }
-  if (kOutOfLine && (diff | (uint32_t)(s0.slow_all | s1.slow_all))) {
+  if (kOutOfLine && (s0.slow_all | s1.slow_all)) {
     SegVals sv;
 #pragma unroll
     for (int i = 0; i < kPairs; ++i) sv.p[i] = P[i];
     const Words4 r = requant_exact(sv, s0, s1, ts, p.c64, Words4{{w[0], w[1], w[2], w[3]}});
 #pragma unroll
     for (int wi = 0; wi < 4; ++wi) w[wi] = r.w[wi];
+  } else if (kOutOfLine && diff) {
+#pragma unroll
+    for (int wi = 0; wi < 4; ++wi) {
+      const float dec = wi < 2 ? s0.dec : s1.dec;
+      uint32_t d = dw[wi];
+#pragma unroll 1
+      while (d) {
+        const int t = (__ffs(d) - 1) >> 2;     // nibble = element of the word
+        d &= ~(0xFu << (4 * t));
+        u64 pr = P[4 * wi];
+#pragma unroll
+        for (int z = 1; z < 4; ++z) pr = (t >> 1) == z ? P[4 * wi + z] : pr;
+        const float x = (t & 1) ? hi_of(pr) : lo_of(pr);
+        const uint32_t c = c_pow2 && fabsf(x) >= 0x1p-100f ? fp4_code_fma(x, (float)p.c64, ts, dec)
+                                                            : fp4_code_exact(x, p.c64, ts, dec);
+        w[wi] = (w[wi] & ~(0xFu << (4 * t))) | (c << (4 * t));
+      }
+    }
   }
   if (!kOutOfLine && (diff | (uint32_t)(s0.slow_all | s1.slow_all))) {
 #pragma unroll

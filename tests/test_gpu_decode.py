@@ -87,3 +87,77 @@ def test_non_decode_shapes_fall_back_to_two_kernels():
         x = torch.randn(M, K, device="cuda").bfloat16()
         assert not decode_eligible(M, w, x.dtype)
         assert torch.equal(P.quantized_linear(x, w), two_kernel(x, w, torch.bfloat16))
+
+
+E4M3_VALUES = [0.5, 0.625, 0.75, 1.0, 1.125, 1.5, 1.75, 2.0, 2.5, 3.0, 3.5, 4.0, 6.0, 8.0, 12.0, 16.0]
+E4M3_POW2 = [0.5, 1.0, 2.0, 4.0, 8.0, 16.0]
+E4M3_MIDS = [0.53125, 0.6875, 1.0625, 1.1875, 1.4375, 1.9375, 2.125, 2.375, 3.25, 3.75, 4.25, 6.5, 7.5, 13.0]
+FP4_T = [0.25, 0.75, 1.25, 1.75, 2.5, 3.5, 5.0]
+
+
+def tie_rows(k, M, K, rng):
+    """NVFP4 activations built so that s_T = 1 exactly (one |y| = 2688 = 6 * 448) and every
+    16-group's scale ratio amax / 6 is an E4M3 value with elements at T * dec for the E2M1
+    rounding thresholds T (element ties), or an E4M3 midpoint (scale ties).  k = 0: directly;
+    k = 16: each block holds two nonzeros a, b, whose rotation has |y| in {(a+b)/4, |a-b|/4}."""
+    X = np.zeros((M, K))
+    for r in range(M):
+        for g in range(K // 16):
+            tie_scale = (r + g) % 2 == 1
+            T = rng.choice(FP4_T)
+            if k == 0:
+                d = rng.choice(E4M3_MIDS if tie_scale else E4M3_VALUES)
+                grp = rng.integers(-5, 6, size=16) * d                     # |.| < 6 d, bf16-exact
+                if not tie_scale:
+                    idx = rng.choice(16, size=7, replace=False)
+                    grp[idx] = np.asarray(FP4_T) * d * rng.choice([-1, 1], size=7)
+                grp[rng.integers(16)] = 6 * d * rng.choice([-1, 1])
+                X[r, 16 * g:16 * g + 16] = grp
+            else:
+                if tie_scale:   # a + b = 24 M (amax / 6 = M, a midpoint), a - b small
+                    m = rng.choice(E4M3_MIDS)
+                    q = 2.0 ** (np.floor(np.log2(m)) - 2) * rng.integers(1, 4)
+                    a, b = 12 * m + q, 12 * m - q
+                else:           # a + b = 24 d (amax = 6 d), a - b = 4 T d (|y| = T d)
+                    d = rng.choice(E4M3_POW2)
+                    a, b = (12 + 2 * T) * d, (12 - 2 * T) * d
+                p0, p1 = rng.choice(16, size=2, replace=False)
+                X[r, 16 * g + p0], X[r, 16 * g + p1] = a * rng.choice([-1, 1]), b * rng.choice([-1, 1])
+    X[0, :16] = 0.0
+    X[0, 0] = 2688.0 * (4 if k == 16 else 1)                         # max |y| = 2688 -> s_T = 1
+    assert np.array_equal(O.bf16_round(X), X)
+    return X
+
+
+@pytest.mark.parametrize("k", [0, 16])
+def test_decode_exact_on_ties(k):
+    """Exact rounding ties everywhere (tie_rows): the decode kernel's division-free re-decisions
+    (fma paths, k in {0, 16}) run on thousands of E2M1 / E4M3 midpoints.  K1's codes equal the
+    oracle's bit for bit on this input, and the decode output equals the K1 + K2 path's (a
+    single code flip would move it by ~1e-3)."""
+    rng = np.random.default_rng(100 + k)
+    M, K, N, fmt = 16, 4096, 1024, "nvfp4"
+    X = tie_rows(k, M, K, rng)
+    Aq = O.quantize_rtn(X, fmt, hadamard=k or None)
+    assert Aq.tensor_scale == 1.0
+    Y = O.rotate_blockwise(X, k or None)
+    amax = np.abs(Y.reshape(M, -1, 16)).max(axis=2)
+    assert np.isin(amax / 6, E4M3_MIDS).sum() > 1000                      # scale ties
+    u = np.abs(Y.reshape(M, -1, 16)) / O.E4M3_LEVELS[Aq.scale_codes.astype(int)][:, :, None]
+    assert np.isin(u, FP4_T).sum() > 1000                                  # element ties
+    W = O.bf16_round(rng.standard_normal((N, K)) / np.sqrt(K))
+    tr = P.TransformSpec.hadamard(k) if k else None
+    w = P.quantize_weight(torch.from_numpy(W).cuda().bfloat16(), SPEC[fmt], tr)
+    x = torch.from_numpy(X).cuda().bfloat16()
+    assert decode_eligible(M, w, x.dtype)
+    a = alloc_result(M, K, w.fmt, w.had_k, x.device)
+    act_quant_into(x, w.fmt, w.had_k, a.codes, a.sf, a.tensor_scale_dev, a.scratch)
+    codes = O.unpack_nibbles(a.codes.cpu().numpy(), M * K).reshape(M, K)
+    from paper_2509_23202_b200 import _lib
+    sf = torch.empty((M, K // 16), dtype=torch.uint8, device="cuda")
+    _lib.check(_lib.lib().mrfp4_sf_unswizzle(_lib.ptr(a.sf), _lib.ptr(sf), M, K // 16, _lib.stream_ptr(torch)))
+    assert np.array_equal(sf.cpu().numpy(), Aq.scale_codes.reshape(M, K // 16))
+    assert np.array_equal(codes, Aq.element_codes.reshape(M, K))
+    y = P.quantized_linear(x, w, out_dtype=torch.float32).cpu().numpy()
+    y2 = two_kernel(x, w, torch.float32).cpu().numpy()
+    assert rel_fro(y, y2) <= 1e-6
