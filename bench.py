@@ -18,7 +18,8 @@ Reported (one JSON line from rank 0):
   cpu_baseline          the CPU oracle (numpy port of the reference) on a bounded sample
   extras                cuBLAS-bf16 time of the same layer and the layer speedup over it,
                         rot+quant GB/s, clocks sampled during the timed region
---impl reference runs the CPU oracle (numpy restatement of microfp) on all host cores.
+--impl reference times the stock reference (microfp staged into oracle/_ref by oracle/make_ref.py;
+the numpy port when absent) on the host cores.
 """
 
 from __future__ import annotations
@@ -113,43 +114,94 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- CPU arms
-def cpu_linear_step(X, Wdeq, fmt, had, workers):
-    import oracle as O
-    q = O.quantize_rtn_parallel(X, fmt, had, workers=workers)
-    return O.dequantize_f32(q) @ Wdeq.T
+def load_reference():
+    """The stock reference package staged into oracle/_ref by oracle/make_ref.py, or None."""
+    ref = os.path.join(ROOT, "oracle", "_ref")
+    if not os.path.isdir(os.path.join(ref, "microfp")):
+        return None
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    import microfp
+    return microfp
 
 
-def cpu_inputs(M, K, N, fmt, had, seed=1234):
-    import numpy as np
-    import oracle as O
-    rng = np.random.default_rng(seed)
-    X = O.bf16_round(rng.standard_normal((M, K), dtype=np.float32))
-    W = O.bf16_round(rng.standard_normal((N, K), dtype=np.float32) / np.sqrt(K))
-    Wq = O.quantize_rtn_parallel(W, fmt, had)
-    return X, O.dequantize_f32(Wq)
+def blas_threads() -> str:
+    try:
+        from threadpoolctl import threadpool_info
+        return ", ".join(f"{d['internal_api']} {d['num_threads']} threads" for d in threadpool_info())
+    except Exception:  # noqa: BLE001
+        return "unknown"
+
+
+class CpuArm:
+    """One CPU quantized-linear step on a sample of the workload's token rows: the reference's
+    own quantize_rtn(X, spec, transform) -> dequantize -> float64 matmul with the dequantized
+    weight (kind "reference"), or the numpy port when oracle/_ref is absent (kind "port")."""
+
+    def __init__(self, K, N, fmt, had, seed=1234):
+        import numpy as np
+        import oracle as O
+        self.mf = load_reference()
+        self.kind = "reference" if self.mf is not None else "port"
+        self.fmt, self.had, self.K = fmt, had, K
+        self.rng = np.random.default_rng(seed)
+        W = O.bf16_round(self.rng.standard_normal((N, K), dtype=np.float32) / np.sqrt(K))
+        if self.mf is not None:
+            self.spec = self.mf.FormatSpec.mxfp4() if fmt == "mxfp4" else self.mf.FormatSpec.nvfp4()
+            self.tr = self.mf.TransformSpec.hadamard(had) if had else None
+            self.Wdeq = self.mf.dequantize(self.mf.quantize_rtn(W, self.spec, transform=self.tr).tensor)
+        else:
+            self.Wdeq = O.dequantize_f32(O.quantize_rtn_parallel(W, fmt, had))
+
+    def inputs(self, rows):
+        import numpy as np
+        import oracle as O
+        return O.bf16_round(self.rng.standard_normal((rows, self.K), dtype=np.float32))
+
+    def step(self, X):
+        if self.mf is not None:
+            q = self.mf.quantize_rtn(X, self.spec, transform=self.tr)
+            return self.mf.dequantize(q.tensor) @ self.Wdeq.T
+        import oracle as O
+        return O.dequantize_f32(O.quantize_rtn_parallel(X, self.fmt, self.had)) @ self.Wdeq.T
+
+    def rows_for(self, seconds, cap):
+        """Token rows per step so that one step takes about `seconds`."""
+        import time as _t
+        X = self.inputs(4)
+        self.step(X)
+        t0 = _t.perf_counter()
+        self.step(X)
+        per_row = (_t.perf_counter() - t0) / 4
+        return int(max(1, min(cap, round(seconds / max(per_row, 1e-9)))))
 
 
 def run_reference(args, cfg, rank):
-    """--impl reference: the CPU oracle (numpy restatement of microfp) on all host cores."""
+    """--impl reference: the reference's own CPU implementation of the path (oracle/_ref, the
+    stock microfp package), each step a bounded sample of the workload's token rows sized so the
+    whole --warmup W --steps K run takes about two minutes; rank 0 only."""
     if rank != 0:
         return
     name, M, K, N, fmt, had = cfg
-    cores = len(os.sched_getaffinity(0))
-    X, Wdeq = cpu_inputs(M, K, N, fmt, had)
+    arm = CpuArm(K, N, fmt, had)
+    rows = arm.rows_for(min(2.0, 120.0 / (args.steps + args.warmup)), M)
+    X = arm.inputs(rows)
     for _ in range(args.warmup):
-        cpu_linear_step(X, Wdeq, fmt, had, cores)
+        arm.step(X)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        cpu_linear_step(X, Wdeq, fmt, had, cores)
+        arm.step(X)
     dt = (time.perf_counter() - t0) / args.steps
-    tflops = 2.0 * M * N * K / dt / 1e12
+    tflops = 2.0 * rows * N * K / dt / 1e12
     line = {
         "impl": "reference", "metric": METRIC, "value": tflops, "unit": "TFLOP/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (bf16 N(0,1) acts, N(0,1/K) weights)",
         "config": {"workload": name, "M": M, "K": K, "N": N, "format": fmt, "hadamard": had},
-        "cpu_baseline": {"value": tflops, "unit": "TFLOP/s", "cores": cores, "kind": "port",
-                         "sample": f"full workload M={M} per step (act-quant + dequant + fp32 matmul)"},
+        "cpu_baseline": {"value": tflops, "unit": "TFLOP/s", "cores": len(os.sched_getaffinity(0)),
+                         "kind": arm.kind, "blas": blas_threads(),
+                         "sample": f"{rows} of the {M} token rows per step, full K and N: quantize_rtn + "
+                                   f"dequantize + float64 matmul ({'stock microfp' if arm.mf else 'numpy port'})"},
         "e2e": {"value": tflops, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -392,18 +444,19 @@ def main():
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:
-        Ms = 256  # bounded sample: 256 of the M tokens, same K/N/format
-        import numpy as np
-        X, Wdeq = cpu_inputs(Ms, K, N, fmt, had)
-        cores = len(os.sched_getaffinity(0))
-        cpu_linear_step(X, Wdeq, fmt, had, cores)
+        arm = CpuArm(K, N, fmt, had)
+        Ms = arm.rows_for(1.0, M)          # bounded sample: ~1 s per step, >= 8 s in all
+        X = arm.inputs(Ms)
+        arm.step(X)
         reps, t0 = 0, time.perf_counter()
-        while reps < 3 or time.perf_counter() - t0 < 5.0:
-            cpu_linear_step(X, Wdeq, fmt, had, cores)
+        while reps < 3 or time.perf_counter() - t0 < 8.0:
+            arm.step(X)
             reps += 1
         tc = (time.perf_counter() - t0) / reps
-        cpu = {"value": 2.0 * Ms * N * K / tc / 1e12, "unit": "TFLOP/s", "cores": cores, "kind": "port",
-               "sample": f"M={Ms} of {M} tokens, act-quant + dequant + fp32 matmul, {reps} reps"}
+        cpu = {"value": 2.0 * Ms * N * K / tc / 1e12, "unit": "TFLOP/s", "cores": len(os.sched_getaffinity(0)),
+               "kind": arm.kind, "blas": blas_threads(),
+               "sample": f"{Ms} of {M} token rows, quantize_rtn + dequantize + float64 matmul, {reps} reps "
+                         f"({'stock microfp from oracle/_ref' if arm.mf else 'numpy port'})"}
 
     if fused_decode:   # the step's one kernel: weight-stream bound (W codes + scales, X in, Y out)
         kd_bytes = k2_bytes + 2.0 * M * K + 4
@@ -427,10 +480,11 @@ def main():
         "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
         "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "fp4-e2m1 (fp32 accum)",
         "data": "synthetic: bf16 N(0,1) activations, N(0,1/K) random-init weights (GPU RTN)",
-        "config": {"workload": name, "M": M, "K": K, "N": N, "format": fmt, "hadamard": had,
-                   "parallelism": f"N-shard x{world}" if sharded else "single",
-                   "gather": gather_used if sharded else None,
-                   "l2": "flushed between steps (256 MiB memset + 256 MiB read sweep)"},
+        # config: the workload only, key for key the reference arm's (run details below)
+        "config": {"workload": name, "M": M, "K": K, "N": N, "format": fmt, "hadamard": had},
+        "parallelism": f"N-shard x{world}" if sharded else "single",
+        "gather": gather_used if sharded else None,
+        "l2": "flushed between steps (256 MiB memset + 256 MiB read sweep)",
         "k1_us": k1_mean * 1e6, "k2_us": k2_mean * 1e6,
         "gather_ms_per_step": {k_: v_ * 1e3 for k_, v_ in t_var.items()} if sharded else None,
         "gemm_tflops_per_gpu": k2_flops / k2_mean / 1e12,

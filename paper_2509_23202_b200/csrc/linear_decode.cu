@@ -154,6 +154,9 @@ __global__ void __launch_bounds__(kDecThreads, 1)
     if (g.trace && threadIdx.x == 0) g.trace[blockIdx.x * 16 + i] = globaltimer();
   };
   stamp(0);
+  // the weight's tensor scale: a weight constant like the codes the TMA prefetches before the
+  // PDL wait (prepare_weight orders it behind its producer); loaded now, used in the epilogue
+  const float w_ts = __ldg(g.w_ts);
 
   if (warp == 0 && lane == 0) {
     sm100::tma_prefetch_desc(&tmW);
@@ -421,7 +424,7 @@ __global__ void __launch_bounds__(kDecThreads, 1)
   {
     // rolled loops: this code runs once per launch, and after an L2 flush every instruction of
     // it is fetched from HBM on the critical path -- fewer is faster
-    const float alpha = k.st32 * __ldg(g.w_ts);
+    const float alpha = k.st32 * w_ts;
 #pragma unroll 1
     for (int e = threadIdx.x; e < g.M * rows_own; e += kDecThreads) {
       const int m = e / rows_own, nloc = e - m * rows_own;
