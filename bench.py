@@ -217,6 +217,8 @@ def main():
     ap.add_argument("--config", default="c1", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-sustained", action="store_true")
+    ap.add_argument("--no-comparators", action="store_true")
     ap.add_argument("--M", type=int, default=0, help="override the config's token count (sweeps)")
     ap.add_argument("--gather", default="auto", choices=["auto", "nccl", "fused"],
                     help="N-sharded output gather: NCCL all-gather, the K2 epilogue's peer stores into "
@@ -442,6 +444,36 @@ def main():
         except Exception:
             traffic = None
 
+    # ---------------- sustained: the same step back to back for >= 4 s (SURVEY.md 8(d) "4 s
+    # loop"; the headline above is the burst-clock figure), clocks sampled over the loop
+    sustained = None
+    if world == 1 and not args.no_sustained:
+        samp = ClockSampler(torch.cuda.current_device()).start(keep_busy=busy)
+        dev_s, n_s, t_wall = 0.0, 0, time.perf_counter()
+        while time.perf_counter() - t_wall < 4.0:
+            ev_s = timed(step, 100)
+            torch.cuda.synchronize(dev)
+            dev_s += sum(a_.elapsed_time(b_) * 1e-3 for a_, b_ in ev_s)
+            n_s += len(ev_s)
+        sustained = {"seconds": time.perf_counter() - t_wall, "steps": n_s, "ms_per_step": dev_s / n_s * 1e3,
+                     "value": flops / (dev_s / n_s) / 1e12, "unit": "TFLOP/s", "clocks": samp.stop(),
+                     "note": "L2 flushed between steps as in the timed region"}
+
+    # ---------------- same-box FP4 comparators on THIS step's operands (
+    # context, not parity oracles): cuBLASLt / flashinfer / vLLM-CUTLASS / QuTLASS GEMMs and the
+    # QuTLASS rotate + quantize kernels
+    comparators = None
+    if world == 1 and not args.no_comparators:
+        try:
+            sys.path.insert(0, os.path.join(ROOT, "scripts"))
+            import fp4_comparators
+            act_quant_into(x, w.fmt, had, a.codes, a.sf, a.tensor_scale_dev, a.scratch)
+            comparators = fp4_comparators.run(x, a, w, fmt, had, flush_l2)
+            comparators["ours_k2"] = {"us": k2_mean * 1e6, "tflops": k2_flops / k2_mean / 1e12}
+            comparators["ours_k1"] = {"us": k1_mean * 1e6, "gbs": k1_bytes / k1_mean / 1e9}
+        except Exception as e:  # noqa: BLE001 - optional context
+            comparators = {"error": f"{type(e).__name__}: {str(e)[:200]}"}
+
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         arm = CpuArm(K, N, fmt, had)
@@ -494,7 +526,7 @@ def main():
         "roofline": k2_roof,
         "roofline_k1": {"bound": "hbm", "kernel": "k_act_quant (K1)", "achieved": k1_bytes / k1_mean / 1e9,
                         "peak": hbm, "unit": "GB/s", "frac": k1_bytes / k1_mean / 1e9 / hbm},
-        "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+        "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "sustained": sustained, "comparators": comparators,
         "gpu_launches": launches_per_step * args.steps,
     }
     print(json.dumps(line), flush=True)

@@ -46,6 +46,11 @@ def run(x, a, w, fmt: str, had: int, flush, n: int = 20) -> dict:
     a4 = a.codes.view(torch.float4_e2m1fn_x2) if hasattr(torch, "float4_e2m1fn_x2") else None
     b4 = w.codes.view(torch.float4_e2m1fn_x2) if a4 is not None else None
     alpha = (a.tensor_scale_dev * w.tensor_scale_dev).contiguous()
+    # the swizzled scale-factor buffers as the 2-D [rows padded to 128, K/G padded to 4] matrices
+    # the libraries index (the bytes are already their 128x4 block-scaled layout)
+    cols = ((K // G) + 3) // 4 * 4
+    sa2 = a.sf.view(-1)[:((M + 127) // 128 * 128) * cols].view((M + 127) // 128 * 128, cols)
+    sb2 = w.sf.view(-1)[:((N + 127) // 128 * 128) * cols].view((N + 127) // 128 * 128, cols)
 
     def gemm_entry(name, fn):
         try:
@@ -54,24 +59,31 @@ def run(x, a, w, fmt: str, had: int, flush, n: int = 20) -> dict:
             t = _time(fn, flush, n, stream)
             out[name] = {"us": t * 1e6, "tflops": flops / t / 1e12}
         except Exception as e:  # noqa: BLE001 - comparators are optional context
-            out[name] = {"error": f"{type(e).__name__}: {str(e)[:160]}"}
+            out[name] = {"error": f"{type(e).__name__}: {str(e)[:600]}"}
 
     if a4 is not None and sf_dtype is not None:
-        sa, sb = a.sf.view(sf_dtype), w.sf.view(sf_dtype)
-        gemm_entry("cublaslt_fp4", lambda: torch._scaled_mm(a4, b4.t(), sa, sb, out_dtype=torch.bfloat16))
+        sa, sb = sa2.view(sf_dtype), sb2.view(sf_dtype)
+        if fmt == "nvfp4":   # alpha applied by _scaled_mm's scale_result is not available: fold later
+            gemm_entry("cublaslt_fp4", lambda: torch._scaled_mm(a4, b4.t(), sa.view(-1), sb.view(-1),
+                                                                out_dtype=torch.bfloat16))
+        else:
+            gemm_entry("cublaslt_fp4", lambda: torch._scaled_mm(a4, b4.t(), sa.view(-1), sb.view(-1),
+                                                                out_dtype=torch.bfloat16))
+            if "error" in out["cublaslt_fp4"]:
+                gemm_entry("cublaslt_fp4", lambda: torch._scaled_mm(a4, b4.t(), sa, sb, out_dtype=torch.bfloat16))
     try:
         import flashinfer
-        sa8 = a.sf.view(torch.float8_e4m3fn if fmt == "nvfp4" else torch.uint8)
-        sb8 = w.sf.view(torch.float8_e4m3fn if fmt == "nvfp4" else torch.uint8)
+        sa8 = sa2.view(torch.float8_e4m3fn if fmt == "nvfp4" else torch.uint8)
+        sb8 = sb2.view(torch.float8_e4m3fn if fmt == "nvfp4" else torch.uint8)
         gemm_entry("flashinfer_fp4", lambda: flashinfer.mm_fp4(
-            a.codes, w.codes.t(), sa8, sb8, alpha, torch.bfloat16, block_size=G, use_nvfp4=fmt == "nvfp4"))
+            a.codes, w.codes.t(), sa8, sb8.t(), alpha, torch.bfloat16, block_size=G, use_nvfp4=fmt == "nvfp4"))
     except Exception as e:  # noqa: BLE001
         out["flashinfer_fp4"] = {"error": f"{type(e).__name__}: {str(e)[:160]}"}
     try:
         import vllm._custom_ops as ops
         if fmt == "nvfp4":
             gemm_entry("vllm_cutlass_nvfp4", lambda: ops.cutlass_scaled_fp4_mm(
-                a.codes, w.codes, a.sf.view(torch.float8_e4m3fn), w.sf.view(torch.float8_e4m3fn), alpha,
+                a.codes, w.codes, sa2.view(torch.float8_e4m3fn), sb2.view(torch.float8_e4m3fn), alpha,
                 torch.bfloat16))
         else:
             gemm_entry("qutlass_mxf4", lambda: ops.matmul_mxf4_bf16_tn(

@@ -4,7 +4,7 @@ tag=${1:-x}
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests/test_gpu_gemm.py tests/test_gpu_fullsize.py tests/test_gpu_configs.py -m gpu -q -x 2>&1 | tail -3 > gpurun_out/${tag}_pytest.log
 for c in c2-up-nv c1 c2-down-mx; do MRFP4_LIB=build/trace/libmrfp4.so timeout 120 python scripts/k2_timeline.py $c; done > gpurun_out/${tag}_timeline.txt 2>&1
-for c in c1 c2-up-nv c2-down-mx c3-gateup; do timeout 300 python bench.py --config $c --steps 200 --warmup 10 --no-cpu-baseline --no-e2e >> gpurun_out/${tag}_bench.jsonl 2>>gpurun_out/${tag}_bench.err; done
+for c in c1 c2-up-nv c2-down-mx c3-gateup; do timeout 300 python bench.py --config $c --steps 200 --warmup 10 --no-cpu-baseline --no-e2e --no-sustained --no-comparators >> gpurun_out/${tag}_bench.jsonl 2>>gpurun_out/${tag}_bench.err; done
 cat gpurun_out/${tag}_pytest.log gpurun_out/${tag}_timeline.txt
 python - "$tag" <<'PY'
 import json, sys

@@ -14,10 +14,10 @@ timeout 300 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/b
 timeout 200 python scripts/decode_probe.py > gpurun_out/decode_probe.txt 2>&1
 for cfg in c1 c0; do
   timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 60 --csv \
-    --log-file gpurun_out/launches_$cfg.csv python bench.py --config $cfg --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_launch_$cfg.log 2>&1
+    --log-file gpurun_out/launches_$cfg.csv python bench.py --config $cfg --steps 5 --warmup 3 --no-cpu-baseline --no-e2e --no-sustained --no-comparators > gpurun_out/ncu_launch_$cfg.log 2>&1
 done
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_gemm -s 3 -c 1 -f -o gpurun_out/prof_k_gemm_c0 \
-  python bench.py --config c0 --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_k_gemm_c0.log 2>&1
+  python bench.py --config c0 --steps 3 --warmup 3 --no-cpu-baseline --no-e2e --no-sustained --no-comparators > gpurun_out/ncu_k_gemm_c0.log 2>&1
 ncu -i gpurun_out/prof_k_gemm_c0.ncu-rep --page details --csv > gpurun_out/prof_k_gemm_c0_details.csv 2>/dev/null
 rm -f gpurun_out/prof_k_gemm_c0.ncu-rep
 ls -la gpurun_out

@@ -6,7 +6,7 @@ out=gpurun_out/${tag}_sweep_70b.jsonl
 : > $out
 for c in c2-up-nv c2-up-mx c2-down-nv c2-down-mx; do
   for m in ${MS:-1 16 128 512 1024 2048 4096 8192}; do
-    timeout 300 python bench.py --config $c --M $m --steps 50 --warmup 5 --no-cpu-baseline --no-e2e >> $out 2>/dev/null
+    timeout 300 python bench.py --config $c --M $m --steps 50 --warmup 5 --no-cpu-baseline --no-e2e --no-sustained --no-comparators >> $out 2>/dev/null
   done
 done
 python - $out <<'PY'
