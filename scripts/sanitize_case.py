@@ -1,7 +1,8 @@
 """Small invocations of every kernel family for compute-sanitizer (scripts/sanitize.sh):
 K1 (MXFP4 single pass, NVFP4 two-phase grid barrier, NVFP4 static s_T, butterfly fp32 path),
-K2 (1-CTA split-K with in-kernel reduction, 2-CTA cta_group::2), the requant epilogue, the
-float64 path, the GPTQ block solver.  Prints one line per case."""
+K2 (1-CTA split-K with in-kernel reduction, 2-CTA cta_group::2), the one-kernel decode linear
+(M <= 32: cluster DSMEM st.async exchanges), the requant epilogue, the float64 path, the GPTQ
+block solver.  Prints one line per case."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -14,7 +15,7 @@ for spec, k in ((MX, 32), (NV, 16)):
     tr = P.TransformSpec.hadamard(k)
     W = (torch.randn(512, 1024, device="cuda") / 32).bfloat16()
     w = P.quantize_weight(W, spec, tr)
-    for M in (16, 300):
+    for M in (1, 16, 32, 100, 300):   # 1/16/32: k_linear_decode; 100: 1-CTA K2; 300: 2-CTA K2
         x = torch.randn(M, 1024, device="cuda").bfloat16()
         y = P.quantized_linear(x, w, check=True)
         torch.cuda.synchronize()
