@@ -228,9 +228,11 @@ int mrfp4_mse_pass(const double* y, int64_t ngroups, int fmt, const double* cand
 int mrfp4_mse_group_err(const double* y, int64_t ngroups, int fmt, const double* decoded, double ts,
                         double* group_err, uint32_t* status, void* stream);
 /*
- * Decode-sized quantized linear in one kernel (M <= 32 tokens): the activation rotate +
- * quantize of mrfp4_act_quant runs inside the GEMM CTAs (each CTA reduces the NVFP4 global
- * scale over the whole, tiny, activation itself -- no grid barrier), and the FP4 GEMM puts the
+ * Decode-sized quantized linear in one kernel (M <= 32 tokens) -- replaces
+ * dequantize(quantize_rtn(X, spec, H_k)) @ dequantize(Wq).T (quantizers.py:247-255,
+ * formats.py:424-442) like mrfp4_act_quant + mrfp4_gemm: the activation rotate + quantize runs
+ * inside the GEMM CTAs (the CTAs of one cluster cover all of K, so the NVFP4 whole-tensor max is
+ * their slice maxima combined over DSMEM -- no grid barrier), and the FP4 GEMM puts the
  * weight on the 128-row MMA side (D^T = W . Xq^T, N = 16 | 32 tokens).  Same result as
  * mrfp4_act_quant + mrfp4_gemm up to fp32 summation order.  x: [M, K] contiguous bf16 / f16;
  * w: [N, K/2] codes + swizzled scales + device tensor scale; d: [M, N] (row stride ldd) bf16 /
