@@ -440,7 +440,7 @@ def main():
     prof = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get(f"{args.config}:k2")
+            traffic = json.load(open(prof)).get(f"{args.config}:{'kd' if fused_decode else 'k2'}")
         except Exception:
             traffic = None
 

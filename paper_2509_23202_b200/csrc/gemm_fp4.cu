@@ -238,8 +238,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // perf traces (null in production): per-CTA globaltimer stamps, 8 slots
-  auto mark = [&](int i) { if (g.dbg) g.dbg[blockIdx.x * 8 + i] = globaltimer(); };
+  // perf experiments (per-CTA globaltimer stamps, load/MMA knock-out modes) exist only in
+  // MRFP4_TRACE builds (scripts/build_variant.sh): compiled out of the production kernel
+#ifdef MRFP4_TRACE
+  const int dbg_mode = g.debug;
+  unsigned long long* const dbg_buf = g.dbg;
+#else
+  constexpr int dbg_mode = 0;
+  unsigned long long* const dbg_buf = nullptr;
+#endif
+  auto mark = [&](int i) { if (dbg_buf) dbg_buf[blockIdx.x * 8 + i] = globaltimer(); };
   if (threadIdx.x == 0) mark(0);
   if (warp == 0 && lane == 0) {
     sm100::tma_prefetch_desc(&tmA);
@@ -287,7 +295,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // The weight half of the first unit's first stages does not depend on the act-quant
       // kernel: issue it before the PDL wait so the weight stream overlaps K1's tail.
       int pre = 0;
-      if (blockIdx.x < num_units && g.debug == 0) {
+      if (blockIdx.x < num_units && dbg_mode == 0) {
         const int tile = blockIdx.x / g.splits, split = blockIdx.x - tile * g.splits;
         const int n_blk = tile / g.num_m_blk;
         const int kb0 = split * g.kb_per, kb1 = min(g.num_kb, kb0 + g.kb_per);
@@ -309,7 +317,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const bool preissued = unit == (int)blockIdx.x && kb - kb0 < pre;
           if (!preissued) sm100::mbar_wait(&empty[stage], phase ^ 1);
           const int atoms = (int)imin64(C::kAtomsPerKb, g.sf_col_blocks - (int64_t)kb * C::kAtomsPerKb);
-          if (g.debug == 1 || g.debug == 3 || g.debug == 4 || g.debug == 5) {
+          if (dbg_mode == 1 || dbg_mode == 3 || dbg_mode == 4 || dbg_mode == 5) {
             sm100::mbar_arrive(&full[stage]);
             if (++stage == C::kStages) { stage = 0; phase ^= 1; }
             continue;
@@ -348,7 +356,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t sfb_s = sm100::smem_u32(smem + C::kOffSfb + stage * C::kSfbBytes);
 #pragma unroll
           for (int a = 0; a < C::kAtomsPerKb; ++a) {
-            if (g.debug < 5 || (g.debug == 6 && kb < C::kStages)) {
+            if (dbg_mode < 5 || (dbg_mode == 6 && kb < C::kStages)) {
               sm100::tc_cp_32x128b_warpx4(sfa_t + a * 4, sm100::smem_desc(sfa_s + a * 512, 0, 128, 0));
 #pragma unroll
               for (int j = 0; j < C::kNB; ++j)
@@ -358,7 +366,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           const uint64_t ad = desc_add(adesc0, (uint32_t)(stage * (C::kABytes >> 4)));
           const uint64_t bd = desc_add(bdesc0, (uint32_t)(stage * (C::kBBytes >> 4)));
-          if (g.debug == 2 || g.debug == 4) {
+          if (dbg_mode == 2 || dbg_mode == 4) {
           } else if (kb + 1 < g.num_kb || g.tail_mmas == 0) {
             issue_kblock<VEC, BK / UMMA_K, BM, BN, C::kNB, false>(tmem_base, ad, bd, sfa_t, sfb_t, kb == kb0);
           } else {
@@ -387,7 +395,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // Split-K: lanes past M skip the TMEM read entirely when the whole warp is past M.
       const bool warp_live = (int64_t)m_blk * BM + q * 32 < g.M;
 #pragma unroll 1
-      for (int c = 0; c < ((g.debug >= 3 && g.debug <= 5) || !warp_live ? 0 : BN); c += 64) {
+      for (int c = 0; c < ((dbg_mode >= 3 && dbg_mode <= 5) || !warp_live ? 0 : BN); c += 64) {
         uint32_t r[2][32];   // two 32-column TMEM loads per wait
         sm100::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + c, r[0]);
         sm100::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + c + 32, r[1]);

@@ -150,8 +150,14 @@ __global__ void __launch_bounds__(kDecThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tile = blockIdx.x / g.splits, split = (int)sm100::cluster_ctarank();   // cluster = one row tile
   const int kb0 = split * g.kb_per, kb1 = min(g.num_kb, kb0 + g.kb_per), nst = kb1 - kb0;
+  // per-CTA globaltimer stamps (scripts/decode_trace.py): MRFP4_TRACE builds only
+#ifdef MRFP4_TRACE
+  unsigned long long* const trace = g.trace;
+#else
+  unsigned long long* const trace = nullptr;
+#endif
   auto stamp = [&](int i) {   // slots 0..15
-    if (g.trace && threadIdx.x == 0) g.trace[blockIdx.x * 16 + i] = globaltimer();
+    if (trace && threadIdx.x == 0) trace[blockIdx.x * 16 + i] = globaltimer();
   };
   stamp(0);
   // the weight's tensor scale: a weight constant like the codes the TMA prefetches before the
@@ -209,146 +215,117 @@ __global__ void __launch_bounds__(kDecThreads, 1)
   pdl_trigger();
   stamp(1);
 
-  // 2. rotate this CTA's K-slice of every token (kept in registers: <= kDecSegs segments per
+  // 2. rotate this CTA's K-slice of every token (kept in registers: kDecSegs segments per
   // thread, all loads of a thread in flight at once); NVFP4: the slice's max |y|, then the
-  // cluster's (= the whole tensor's) over DSMEM.  3. the slice -> SMEM operand (128-B swizzled
-  // K-major) + SF atoms.
-  //
-  // Both run twice over the same instructions: pass 0 on dummy data (all ones, fixed encode
-  // constants) while the activation loads are in flight, pass 1 on the activations.  After an
-  // L2 flush the kernel's code comes from HBM line by line as it first executes; pass 0 takes
-  // those misses under the load latency instead of on the critical path.  Pass 0 writes exactly
-  // the SMEM locations pass 1 overwrites, and its status bits are dropped.
+  // cluster's (= the whole tensor's) over DSMEM.
   const int nseg_slice = nst * 8;                 // 256 FP4 per stage = 8 segments of 32
-  uint4 v[kDecSegs][4];
-#pragma unroll
-  for (int b = 0; b < kDecSegs; ++b) {
-    const int s = threadIdx.x + b * kDecThreads;
-    const int r = s / nseg_slice, cs = s - r * nseg_slice;
-    const uint4* src = reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(g.x) + (int64_t)r * g.K +
-                                                      (int64_t)(kb0 * 256 + cs * kSeg));
-#pragma unroll
-    for (int c = 0; c < 4; ++c) v[b][c] = r < g.M ? __ldg(src + c) : make_uint4(0, 0, 0, 0);
-  }
-  if (warp == 0 && lane == 0)
-    for (int j = kEarly; j < min(nst, kDecStages); ++j) load_stage(j);
-  uint32_t bad = 0;
-  EncConsts k;                                     // pass 0: s_T = 1 (NVFP4), 4/3 (MXFP4)
-  if constexpr (FMT == MRFP4_FMT_NVFP4) {
-    k.st32 = 1.f;
-    k.st64 = 1.0;
-    k.kenc = (float)(g.qp.c64 / 6.0);
-    k.knv = (float)g.qp.c64;
-  } else {
-    k.st32 = g.qp.mx_ts;
-  }
-#ifndef MRFP4_DEC_WARM
-#define MRFP4_DEC_WARM 0   // measured: the dummy pass costs more than the code misses it hides
-#endif
-#pragma unroll 1
-  for (int pass = 1 - MRFP4_DEC_WARM; pass < 2; ++pass) {
-    u64 P[kDecSegs][kPairs];
-    if (pass) {
-#pragma unroll
-      for (int b = 0; b < kDecSegs; ++b)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const uint32_t w[4] = {v[b][c].x, v[b][c].y, v[b][c].z, v[b][c].w};
-#pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            if constexpr (IN == MRFP4_DT_BF16) {
-              P[b][4 * c + t] = pk(__uint_as_float(w[t] << 16), __uint_as_float(w[t] & 0xFFFF0000u));
-            } else {
-              const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[t]));
-              P[b][4 * c + t] = pk(f.x, f.y);
-            }
-          }
-        }
-    } else {
-#pragma unroll
-      for (int b = 0; b < kDecSegs; ++b)
-#pragma unroll
-        for (int i = 0; i < kPairs; ++i) P[b][i] = pk(1.f, 1.f);
-    }
-    if constexpr (HK > 0) {
-#pragma unroll
-      for (int b = 0; b < kDecSegs; ++b) fwht<HK>(P[b], 0, g.qp.pm);
-    }
-    if (pass) {
-      stamp(6);
-      asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
-      stamp(8);
-      if constexpr (FMT == MRFP4_FMT_NVFP4) {
-        float m = 0.f;
-#pragma unroll
-        for (int b = 0; b < kDecSegs; ++b) {   // rows >= M were zero-filled: |0| adds nothing
-          float a0, a1;
-          half_amax(P[b], a0, a1);
-          m = max3n(a0, a1, m);
-        }
-        uint32_t mb = __float_as_uint(m);
-        mb = mb > 0x7f800000u ? 0x7fc00000u : mb;
-        mb = __reduce_max_sync(0xffffffffu, mb);
-        if (lane == 0) wmax[warp] = mb;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-          uint32_t x = 0;
-          for (int i = 0; i < kDecThreads / 32; ++i) x = max(x, wmax[i]);
-          for (int rr = 0; rr < g.splits; ++rr) st_async_u32(&cmaxs[split], x, &mbar_max, (uint32_t)rr);
-        }
-        stamp(7);
-        if (threadIdx.x == 0) {
-          sm100::mbar_wait(&mbar_max, 0);            // every slice's maximum has landed here
-          stamp(12);
-          uint32_t x = 0;
-          for (int rr = 0; rr < g.splits; ++rr) x = max(x, cmaxs[rr]);
-          sk = nv_consts_fast(g.qp, kPow2C, x);
-          stamp(13);
-        }
-        __syncthreads();
-        k = sk;
-      }
-      stamp(2);
-    }
-
-    uint32_t bq = 0;
+  u64 P[kDecSegs][kPairs];
+  {
+    uint4 v[kDecSegs][4];
 #pragma unroll
     for (int b = 0; b < kDecSegs; ++b) {
       const int s = threadIdx.x + b * kDecThreads;
-      const int r = s / nseg_slice, cs = s - r * nseg_slice;     // token row, segment in the slice
-      if (r >= g.M) continue;
-      const int j = cs >> 3, chunk = cs & 7;                     // stage, 16-B chunk in the 128-B row
+      const int r = s / nseg_slice, cs = s - r * nseg_slice;
+      const uint4* src = reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(g.x) + (int64_t)r * g.K +
+                                                        (int64_t)(kb0 * 256 + cs * kSeg));
+#pragma unroll
+      for (int c = 0; c < 4; ++c) v[b][c] = r < g.M ? __ldg(src + c) : make_uint4(0, 0, 0, 0);
+    }
+    if (warp == 0 && lane == 0)
+      for (int j = kEarly; j < min(nst, kDecStages); ++j) load_stage(j);
+#pragma unroll
+    for (int b = 0; b < kDecSegs; ++b) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const uint32_t w[4] = {v[b][c].x, v[b][c].y, v[b][c].z, v[b][c].w};
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          if constexpr (IN == MRFP4_DT_BF16) {
+            P[b][4 * c + t] = pk(__uint_as_float(w[t] << 16), __uint_as_float(w[t] & 0xFFFF0000u));
+          } else {
+            const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[t]));
+            P[b][4 * c + t] = pk(f.x, f.y);
+          }
+        }
+      }
+      if constexpr (HK > 0) fwht<HK>(P[b], 0, g.qp.pm);
+    }
+  }
+  stamp(6);
+  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+  stamp(8);
+  EncConsts k;
+  if constexpr (FMT == MRFP4_FMT_NVFP4) {
+    float m = 0.f;
+#pragma unroll
+    for (int b = 0; b < kDecSegs; ++b) {   // rows >= M were zero-filled: |0| adds nothing
       float a0, a1;
       half_amax(P[b], a0, a1);
-      GroupScale s0, s1;
-      uint32_t sfc;
-      if constexpr (FMT == MRFP4_FMT_NVFP4) {
-        s0 = nv_group_scale<true>(a0, g.qp, k.kenc, k.knv, k.st32, k.st64, k.zero_code, kPow2C);
-        s1 = nv_group_scale<true>(a1, g.qp, k.kenc, k.knv, k.st32, k.st64, k.zero_code, kPow2C);
-        if (__float_as_uint(a0) >= 0x7f800000u || __float_as_uint(a1) >= 0x7f800000u) bq |= MRFP4_STATUS_NONFINITE;
-        if (s0.code == 0 || s1.code == 0) bq |= MRFP4_STATUS_SCALE_UNDERFLOW;
-        sfc = s0.code | (s1.code << 8);
-      } else {
-        const float a = max3n(a0, a1, 0.f);
-        if (__float_as_uint(a) >= 0x7f800000u) bq |= MRFP4_STATUS_NONFINITE;
-        s0 = mx_group_scale(a, g.qp);
-        s1 = s0;
-        sfc = s0.code;
-      }
-      uint32_t w4[4];
-      quantize_seg<true>(P[b], s0, s1, k.st32, g.qp, w4, kPow2C);
-      *reinterpret_cast<uint4*>(smem + C::kOffX + j * kDecXStage + r * 128 + ((chunk ^ (r & 7)) << 4)) =
-          make_uint4(w4[0], w4[1], w4[2], w4[3]);
-      // SF column of this segment within the stage: NVFP4 2 * chunk (+1), MXFP4 chunk
-      uint8_t* sfst = smem + C::kOffXsf + j * C::kSfStage;
-      const int col = FMT == MRFP4_FMT_NVFP4 ? 2 * chunk : chunk;
-      const int off = (col >> 2) * 512 + (r & 31) * 16 + ((r >> 5) & 3) * 4 + (col & 3);
-      if constexpr (FMT == MRFP4_FMT_NVFP4)
-        *reinterpret_cast<uint16_t*>(sfst + off) = (uint16_t)sfc;
-      else
-        sfst[off] = (uint8_t)sfc;
+      m = max3n(a0, a1, m);
     }
-    if (pass) bad = bq;
+    uint32_t mb = __float_as_uint(m);
+    mb = mb > 0x7f800000u ? 0x7fc00000u : mb;
+    mb = __reduce_max_sync(0xffffffffu, mb);
+    if (lane == 0) wmax[warp] = mb;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t x = 0;
+      for (int i = 0; i < kDecThreads / 32; ++i) x = max(x, wmax[i]);
+      for (int rr = 0; rr < g.splits; ++rr) st_async_u32(&cmaxs[split], x, &mbar_max, (uint32_t)rr);
+    }
+    stamp(7);
+    if (threadIdx.x == 0) {
+      sm100::mbar_wait(&mbar_max, 0);            // every slice's maximum has landed here
+      stamp(12);
+      uint32_t x = 0;
+      for (int rr = 0; rr < g.splits; ++rr) x = max(x, cmaxs[rr]);
+      sk = nv_consts_fast(g.qp, kPow2C, x);
+      stamp(13);
+    }
+    __syncthreads();
+    k = sk;
+  } else {
+    k.st32 = g.qp.mx_ts;
+  }
+  stamp(2);
+
+  // 3. the slice -> SMEM operand (128-B swizzled K-major) + SF atoms
+  uint32_t bad = 0;
+#pragma unroll
+  for (int b = 0; b < kDecSegs; ++b) {
+    const int s = threadIdx.x + b * kDecThreads;
+    const int r = s / nseg_slice, cs = s - r * nseg_slice;     // token row, segment in the slice
+    if (r >= g.M) continue;
+    const int j = cs >> 3, chunk = cs & 7;                     // stage, 16-B chunk in the 128-B row
+    float a0, a1;
+    half_amax(P[b], a0, a1);
+    GroupScale s0, s1;
+    uint32_t sfc;
+    if constexpr (FMT == MRFP4_FMT_NVFP4) {
+      s0 = nv_group_scale<true>(a0, g.qp, k.kenc, k.knv, k.st32, k.st64, k.zero_code, kPow2C);
+      s1 = nv_group_scale<true>(a1, g.qp, k.kenc, k.knv, k.st32, k.st64, k.zero_code, kPow2C);
+      if (__float_as_uint(a0) >= 0x7f800000u || __float_as_uint(a1) >= 0x7f800000u) bad |= MRFP4_STATUS_NONFINITE;
+      if (s0.code == 0 || s1.code == 0) bad |= MRFP4_STATUS_SCALE_UNDERFLOW;
+      sfc = s0.code | (s1.code << 8);
+    } else {
+      const float a = max3n(a0, a1, 0.f);
+      if (__float_as_uint(a) >= 0x7f800000u) bad |= MRFP4_STATUS_NONFINITE;
+      s0 = mx_group_scale(a, g.qp);
+      s1 = s0;
+      sfc = s0.code;
+    }
+    uint32_t w4[4];
+    quantize_seg<true>(P[b], s0, s1, k.st32, g.qp, w4, kPow2C);
+    *reinterpret_cast<uint4*>(smem + C::kOffX + j * kDecXStage + r * 128 + ((chunk ^ (r & 7)) << 4)) =
+        make_uint4(w4[0], w4[1], w4[2], w4[3]);
+    // SF column of this segment within the stage: NVFP4 2 * chunk (+1), MXFP4 chunk
+    uint8_t* sfst = smem + C::kOffXsf + j * C::kSfStage;
+    const int col = FMT == MRFP4_FMT_NVFP4 ? 2 * chunk : chunk;
+    const int off = (col >> 2) * 512 + (r & 31) * 16 + ((r >> 5) & 3) * 4 + (col & 3);
+    if constexpr (FMT == MRFP4_FMT_NVFP4)
+      *reinterpret_cast<uint16_t*>(sfst + off) = (uint16_t)sfc;
+    else
+      sfst[off] = (uint8_t)sfc;
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic SMEM writes -> tcgen05 reads
   sm100::tc_fence_before();
@@ -405,22 +382,22 @@ __global__ void __launch_bounds__(kDecThreads, 1)
   if (warp >= 4 && warp < 8) {
     const int q = warp & 3;
     sm100::mbar_wait(&tfull, 0);
-    if (warp == 4 && lane == 0 && g.trace) g.trace[blockIdx.x * 16 + 4] = globaltimer();
+    if (warp == 4 && lane == 0 && trace) trace[blockIdx.x * 16 + 4] = globaltimer();
     sm100::tc_fence_after();
     uint32_t r[32];
     sm100::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16), r);
     sm100::tmem_ld_wait();
-    if (warp == 4 && lane == 0 && g.trace) g.trace[blockIdx.x * 16 + 9] = globaltimer();
+    if (warp == 4 && lane == 0 && trace) trace[blockIdx.x * 16 + 9] = globaltimer();
     const int nl = q * 32 + lane, owner = nl / rows_own, nloc = nl - owner * rows_own;
     const uint32_t dst = mapa_u32(recv + ((split * rows_own + nloc) * Mp), (uint32_t)owner);
     const uint32_t bar = mapa_u32(&mbar_part, (uint32_t)owner);
 #pragma unroll
     for (int m4 = 0; m4 < 32; m4 += 4)
       if (m4 < Mp) st_async_v4(dst + 4 * m4, r[m4], r[m4 + 1], r[m4 + 2], r[m4 + 3], bar);
-    if (warp == 4 && lane == 0 && g.trace) g.trace[blockIdx.x * 16 + 10] = globaltimer();
+    if (warp == 4 && lane == 0 && trace) trace[blockIdx.x * 16 + 10] = globaltimer();
   }
   sm100::mbar_wait(&mbar_part, 0);               // all S partials of this CTA's rows have landed
-  if (warp == 4 && lane == 0 && g.trace) g.trace[blockIdx.x * 16 + 11] = globaltimer();
+  if (warp == 4 && lane == 0 && trace) trace[blockIdx.x * 16 + 11] = globaltimer();
   {
     // rolled loops: this code runs once per launch, and after an L2 flush every instruction of
     // it is fetched from HBM on the critical path -- fewer is faster
@@ -438,7 +415,7 @@ __global__ void __launch_bounds__(kDecThreads, 1)
     }
   }
   if (bad && g.status) atomicOr(g.status, bad);
-  if (warp == 4 && lane == 0 && g.trace) g.trace[blockIdx.x * 16 + 5] = globaltimer();
+  if (warp == 4 && lane == 0 && trace) trace[blockIdx.x * 16 + 5] = globaltimer();
   sm100::tc_fence_before();
   __syncthreads();
   if (warp == 1) {

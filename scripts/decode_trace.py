@@ -1,4 +1,6 @@
-"""Per-CTA timeline of the fused decode kernel (globaltimer, us from the first CTA start)."""
+"""Per-CTA timeline of the fused decode kernel (globaltimer, us from the first CTA start).
+Needs a trace build: VSRC=linear_decode scripts/build_variant.sh trace_dec -DMRFP4_TRACE, then
+MRFP4_LIB=build/var_trace_dec/libmrfp4.so python scripts/decode_trace.py M K N fmt(0 mx/1 nv) k [noflush]."""
 import ctypes, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
