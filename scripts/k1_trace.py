@@ -32,6 +32,8 @@ q = lambda v: [round(float(torch.quantile(v, z)) / 1000, 2) for z in (0.0, 0.5, 
 print(f"event {s.elapsed_time(e) * 1000:.2f} us, warps {len(t)}, items/warp {n.min().item()}..{n.max().item()}")
 print("start   us q0/50/90/100:", q(st))
 print("end     us:", q(end))
+if (t[:, 3] > 0).any():
+    print("NVFP4 phase-1 end us:", q((t[:, 3] - t0).float()), " barrier released us:", q((t[:, 4] - t0).float()))
 sm = (t[:, 2] >> 32)
 persm = torch.zeros(int(sm.max()) + 1)
 persm.index_reduce_(0, sm, end, "amax", include_self=False)
