@@ -19,10 +19,12 @@
 //      layout plus 128x4 scale-factor atoms (rows >= M zero);
 //   4. one thread issues tcgen05.cp (scale factors) + tcgen05.mma kind::mxf4nvf4 M=128, N=16|32,
 //      K=64 per stage into a TMEM accumulator;
-//   5. the epilogue moves the CTA's fp32 partial D^T into shared memory; after a cluster barrier
-//      CTA r sums rows [r * 128 / S, (r + 1) * 128 / S) of all S partials in rank order over
-//      DSMEM (deterministic), scales by ts_x * ts_w and stores Y[m, n] (coalesced over n).
-// No global workspace, no atomics, no CTA waits on another cluster.
+//   5. the epilogue reads the CTA's fp32 partial D^T from TMEM and pushes each weight row to the
+//      cluster CTA that owns it (st.async ... mbarrier::complete_tx into the owner's shared
+//      memory); CTA r sums rows [r * 128 / S, (r + 1) * 128 / S) of all S partials in rank order
+//      (deterministic), scales by ts_x * ts_w and stores Y[m, n] (coalesced over n).
+// The slice maxima of step 2 travel the same way.  No global workspace, no atomics, no CTA waits
+// on another cluster, and the only cluster barrier is the split arrive / wait at the start.
 #include <cudaTypedefs.h>
 
 #include <algorithm>
