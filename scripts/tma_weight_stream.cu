@@ -1,0 +1,104 @@
+// Weight-stream bandwidth of TMA box shapes (the small-M GEMM's access pattern): a [28672 rows]
+// x [4096 B] FP4 weight (Llama-3-70B up_proj at K = 8192), each CTA (one thread) streaming whole
+// 128-row tiles across all of K through an S-stage ring, no consumer work.  2-D boxes of
+// 128 B x 128 rows (one 128-B piece of each row per box, rows 4 KB apart) vs 3-D boxes of
+// {128 B, 128 rows, n slices} (n consecutive 128-B pieces of each row per box).
+#include <cstdio>
+#include <cstdint>
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+#include "../paper_2509_23202_b200/csrc/sm100.cuh"
+using namespace mrfp4::sm100;
+
+constexpr int kRowBytes = 4096, kRows = 28672, kTileRows = 128;
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* desc, uint64_t* bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+      ::"r"(smem_u32(dst)), "l"(desc), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <int S, int NS>
+__global__ void k_wstream(const __grid_constant__ CUtensorMap tm, int tiles) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t full[S];
+  if (threadIdx.x != 0) return;
+  for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
+  fence_mbar_init();
+  constexpr int box = 128 * kTileRows * NS;
+  const int kpieces = kRowBytes / (128 * NS);
+  // this CTA's boxes: tiles t = blockIdx.x + i * gridDim.x, all k pieces of each
+  const int my_tiles = (tiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+  const int64_t n = (int64_t)my_tiles * kpieces;
+  auto issue = [&](int64_t j, int s) {
+    const int t = (int)blockIdx.x + (int)(j / kpieces) * (int)gridDim.x, kp = (int)(j % kpieces);
+    mbar_arrive_expect_tx(&full[s], box);
+    if (NS == 1) tma_load_2d(smem + s * box, &tm, &full[s], kp * 128, t * kTileRows);
+    else tma_load_3d(smem + s * box, &tm, &full[s], 0, t * kTileRows, kp * NS);
+  };
+  int64_t issued = 0;
+  for (int s = 0; s < S && issued < n; ++s, ++issued) issue(issued, s);
+  uint32_t ph = 0;
+  int s = 0;
+  for (int64_t j = 0; j < n; ++j) {
+    mbar_wait(&full[s], (ph >> s) & 1);
+    ph ^= 1u << s;
+    if (issued < n) { issue(issued, s); ++issued; }
+    s = s + 1 == S ? 0 : s + 1;
+  }
+}
+
+int main() {
+  PFN_cuTensorMapEncodeTiled_v12000 enc;
+  cudaDriverEntryPointQueryResult q;
+  cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&enc, cudaEnableDefault, &q);
+  const size_t bytes = (size_t)kRows * kRowBytes;
+  void* buf; cudaMalloc(&buf, bytes); cudaMemset(buf, 1, bytes);
+  void* fl; cudaMalloc(&fl, 256 << 20);
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  const int tiles = kRows / kTileRows;
+  auto run = [&](auto kern, const CUtensorMap& tm, int smem, int grid, const char* name) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    float best = 1e9;
+    for (int it = 0; it < 5; ++it) {
+      cudaMemset(fl, it, 256 << 20);
+      cudaEventRecord(e0);
+      kern<<<grid, 32, smem>>>(tm, tiles);
+      cudaEventRecord(e1); cudaEventSynchronize(e1);
+      float ms; cudaEventElapsedTime(&ms, e0, e1);
+      if (ms < best) best = ms;
+    }
+    printf("%-34s grid %3d: %7.1f us  %.2f TB/s  %s\n", name, grid, best * 1e3, bytes / (best * 1e-3) / 1e12,
+           cudaGetErrorString(cudaGetLastError()));
+  };
+  CUtensorMap tm2, tm3a, tm3b;
+  cuuint32_t es[3] = {1, 1, 1};
+  {
+    cuuint64_t dims[2] = {kRowBytes, kRows};
+    cuuint64_t strides[1] = {kRowBytes};
+    cuuint32_t box[2] = {128, kTileRows};
+    enc(&tm2, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, buf, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
+  for (int ns : {2, 4}) {
+    cuuint64_t dims[3] = {128, kRows, kRowBytes / 128};
+    cuuint64_t strides[2] = {kRowBytes, 128};
+    cuuint32_t box[3] = {128, kTileRows, (cuuint32_t)ns};
+    enc(ns == 2 ? &tm3a : &tm3b, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, buf, dims, strides, box, es,
+        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
+  for (int grid : {148, 112}) {
+    run(k_wstream<4, 1>, tm2, 4 * 16384 + 1024, grid, "2-D 128Bx128, 4 stages (64 KB)");
+    run(k_wstream<8, 1>, tm2, 8 * 16384 + 1024, grid, "2-D 128Bx128, 8 stages (128 KB)");
+    run(k_wstream<12, 1>, tm2, 12 * 16384 + 1024, grid, "2-D 128Bx128, 12 stages (192 KB)");
+    run(k_wstream<4, 2>, tm3a, 4 * 32768 + 1024, grid, "3-D 128Bx128x2, 4 stages (128 KB)");
+    run(k_wstream<6, 2>, tm3a, 6 * 32768 + 1024, grid, "3-D 128Bx128x2, 6 stages (192 KB)");
+    run(k_wstream<2, 4>, tm3b, 2 * 65536 + 1024, grid, "3-D 128Bx128x4, 2 stages (128 KB)");
+    run(k_wstream<3, 4>, tm3b, 3 * 65536 + 1024, grid, "3-D 128Bx128x4, 3 stages (192 KB)");
+  }
+  return 0;
+}
