@@ -445,6 +445,36 @@ bool decode_plan(int64_t M, int64_t N, int64_t K, int* splits, int* kb_per) {
 
 size_t decode_workspace_bytes(int64_t, int64_t, int64_t) { return 0; }
 
+// One launcher per instantiation: its own per-device attribute cache (a shared generic lambda
+// would share one static between kernels of the same signature).
+template <int IN, int V, int H>
+int launch_decode_kernel(const CUtensorMap& tm, const DecArgs& g, cudaStream_t s) {
+  static std::atomic<int> attr[kMaxDevices];
+  constexpr int smem = DecCfg<V>::kSmem;
+  if (per_device_once(attr, [&] {
+        return cudaFuncSetAttribute(k_linear_decode<IN, V, H>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) ==
+                       cudaSuccess
+                   ? 1
+                   : -1;
+      }) < 0)
+    return MRFP4_ECUDA;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(g.row_tiles * g.splits);
+  cfg.blockDim = dim3(kDecThreads);
+  cfg.dynamicSmemBytes = (size_t)smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr2[2];
+  attr2[0].id = cudaLaunchAttributeClusterDimension;     // one cluster per weight row tile
+  attr2[0].val.clusterDim.x = (unsigned)g.splits;
+  attr2[0].val.clusterDim.y = 1;
+  attr2[0].val.clusterDim.z = 1;
+  attr2[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr2[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr2;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  return cudaLaunchKernelEx(&cfg, k_linear_decode<IN, V, H>, tm, g) == cudaSuccess ? MRFP4_OK : MRFP4_ECUDA;
+}
+
 // Returns MRFP4_EUNSUPPORTED when the shape is not a decode shape (the caller uses K1 + K2).
 int launch_linear_decode(const void* x, int x_dtype, int64_t M, int64_t K, int fmt, int hk, const uint8_t* w,
                          const uint8_t* w_sf, const float* w_ts, int64_t N, void* d, int d_dtype, int64_t ldd,
@@ -493,27 +523,8 @@ int launch_linear_decode(const void* x, int x_dtype, int64_t M, int64_t K, int f
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return MRFP4_ECUDA;
-  auto go = [&](auto kern, int smem) -> int {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
-      return MRFP4_ECUDA;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(g.row_tiles * g.splits);
-    cfg.blockDim = dim3(kDecThreads);
-    cfg.dynamicSmemBytes = (size_t)smem;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[2];
-    attr[0].id = cudaLaunchAttributeClusterDimension;     // one cluster per weight row tile
-    attr[0].val.clusterDim.x = (unsigned)g.splits;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[1].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = pdl_enabled() ? 2 : 1;
-    return cudaLaunchKernelEx(&cfg, kern, tm, g) == cudaSuccess ? MRFP4_OK : MRFP4_ECUDA;
-  };
 #define MRFP4_DEC(IN, V, H) \
-  if (x_dtype == IN && G == V && hk == H) return go(k_linear_decode<IN, V, H>, DecCfg<V>::kSmem);
+  if (x_dtype == IN && G == V && hk == H) return launch_decode_kernel<IN, V, H>(tm, g, s);
   MRFP4_DEC(MRFP4_DT_BF16, 16, 16) MRFP4_DEC(MRFP4_DT_BF16, 16, 32) MRFP4_DEC(MRFP4_DT_BF16, 16, 0)
   MRFP4_DEC(MRFP4_DT_BF16, 32, 16) MRFP4_DEC(MRFP4_DT_BF16, 32, 32) MRFP4_DEC(MRFP4_DT_BF16, 32, 0)
   MRFP4_DEC(MRFP4_DT_F16, 16, 16) MRFP4_DEC(MRFP4_DT_F16, 16, 32) MRFP4_DEC(MRFP4_DT_F16, 16, 0)
