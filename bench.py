@@ -41,6 +41,7 @@ CONFIGS = {
     # name: (workload, M, K, N, fmt, hadamard)
     "c1": ("llama3-8b mlp.down_proj 14336->4096, 2048 tokens, MXFP4+H32", 2048, 14336, 4096, "mxfp4", 32),
     "c0": ("llama3-8b attn.q_proj 4096->4096, 16 tokens, NVFP4+H16", 16, 4096, 4096, "nvfp4", 16),
+    "c0-up": ("llama3-8b mlp.up_proj 4096->14336, 16 tokens, NVFP4+H16", 16, 4096, 14336, "nvfp4", 16),
     "c2-up-nv": ("llama3-70b mlp.up 8192->28672, 2048 tokens, NVFP4+H16", 2048, 8192, 28672, "nvfp4", 16),
     "c2-down-mx": ("llama3-70b mlp.down 28672->8192, 2048 tokens, MXFP4+H32", 2048, 28672, 8192, "mxfp4", 32),
     "c2-up-mx": ("llama3-70b mlp.up 8192->28672, 2048 tokens, MXFP4+H32", 2048, 8192, 28672, "mxfp4", 32),

@@ -18,6 +18,7 @@ int launch_linear_decode(const void* x, int x_dtype, int64_t M, int64_t K, int f
                          void* ws, size_t ws_bytes, uint32_t* status, cudaStream_t s);
 size_t decode_workspace_bytes(int64_t M, int64_t N, int64_t K);
 bool decode_plan(int64_t M, int64_t N, int64_t K, int* splits, int* kb_per);
+bool decode_p_plan(int64_t M, int64_t N, int64_t K, int* grid);
 int launch_gptq_block(double* W, const double* S, const double* T, int64_t rows, int64_t d, int i1, int B, double* Q,
                       uint8_t* codes, double* Err, cudaStream_t s);
 int launch_rotate_f64(const double* x, int64_t M, int64_t K, int64_t ldx, int hk, double* y, cudaStream_t s);
@@ -163,10 +164,11 @@ int mrfp4_rotate_f64(const double* x, int64_t M, int64_t K, int64_t ldx, int had
 }
 
 int mrfp4_linear_decode_ctas(int64_t M, int64_t N, int64_t K) {
-  if (M < 1 || M > 32 || K % 256 || K < 256 || N % 128 || M * K > (1 << 18)) return 0;
-  int sp, per;
-  if (!mrfp4::decode_plan(M, N, K, &sp, &per)) return 0;
-  return (int)(N / 128) * sp;
+  if (M < 1 || M > 32 || K % 256 || K < 256 || N % 128) return 0;
+  int sp, per, grid;
+  if (M * K <= (1 << 18) && mrfp4::decode_plan(M, N, K, &sp, &per)) return (int)(N / 128) * sp;
+  if (mrfp4::decode_p_plan(M, N, K, &grid)) return grid;   // persistent wide-weight variant
+  return 0;
 }
 
 size_t mrfp4_linear_decode_workspace(int64_t M, int64_t N, int64_t K) {

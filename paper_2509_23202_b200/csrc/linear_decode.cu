@@ -67,6 +67,7 @@ struct DecArgs {
   uint32_t* status;
   AQParams qp;              // c64 / kraw / kmx / pm / mx_ts of the activation quantization
   unsigned long long* trace;  // perf experiments: per-CTA globaltimer stamps (null in production)
+  int pgrid;                // k_linear_decode_p: persistent CTAs (row tiles strided over them)
 };
 unsigned long long* g_dec_trace = nullptr;
 
@@ -426,6 +427,265 @@ __global__ void __launch_bounds__(kDecThreads, 1)
   }
 }
 
+
+// ---------------------------------------------------------------------------------------------
+// The same one-kernel decode linear for WIDE weights (more 128-row tiles than one wave of
+// clusters covers: Llama-3-8B gate/up, 70B up at M <= 16, ...): persistent CTAs, no K split.
+// Each CTA quantizes the WHOLE activation once into shared memory (tokens <= 16 | 32 rows,
+// K <= 8192 | 4096: its codes + scale atoms stay resident) -- the NVFP4 whole-tensor max is then
+// CTA-local, no exchange at all -- and streams whole 128-row weight tiles t = blockIdx.x + i *
+// gridDim.x through a 4-stage TMA ring, the MMA alternating two TMEM accumulators so a tile's
+// epilogue (direct Y stores) overlaps the next tile's MMAs.  The weight prefetch starts before
+// the PDL wait and runs under the activation quantization.
+constexpr int kPStages = 4;
+
+template <int VEC>
+struct PCfg {
+  static constexpr int kAtoms = 256 / VEC / 4;
+  static constexpr int kSfStage = kAtoms * 512;
+  static constexpr int kOffW = 0;
+  static constexpr int kOffWsf = kOffW + kPStages * kDecStageCodes;
+  static constexpr int kOffX = kOffWsf + kPStages * kSfStage;     // then nkb x (NT x 128) X codes,
+  static constexpr int kSfCols = 2 * kAtoms * 4;                  // then nkb x kSfStage X scales
+  static constexpr int kSfBase = 64;                              // two 32-column accumulators
+  static int smem(int nkb, int NT) { return kOffX + nkb * (NT * 128 + kSfStage) + 1024; }
+};
+
+template <int IN, int VEC, int HK>
+__global__ void __launch_bounds__(kDecThreads, 1)
+    k_linear_decode_p(const __grid_constant__ CUtensorMap tmW, DecArgs g) {
+  using C = PCfg<VEC>;
+  constexpr int FMT = VEC == 16 ? MRFP4_FMT_NVFP4 : MRFP4_FMT_MXFP4;
+  constexpr bool kPow2C = HK == 0 || HK == 16;
+  constexpr int kQThreads = kDecThreads - 32;   // warps 1.. quantize X; warp 0 is the producer
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t full[kPStages], empty[kPStages], tfull[2], tempty[2];
+  __shared__ uint32_t tmem_holder, wmax[kDecThreads / 32];
+  __shared__ EncConsts sk;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nkb = g.num_kb, NT = g.NT;
+  const int xstage = NT * 128;
+  uint8_t* const xs = smem + C::kOffX;
+  uint8_t* const xsf = xs + nkb * xstage;
+  const float w_ts = __ldg(g.w_ts);
+
+  if (warp == 0 && lane == 0) {
+    sm100::tma_prefetch_desc(&tmW);
+    for (int i = 0; i < kPStages; ++i) {
+      sm100::mbar_init(&full[i], 1);
+      sm100::mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      sm100::mbar_init(&tfull[i], 1);
+      sm100::mbar_init(&tempty[i], 4);
+    }
+    sm100::fence_mbar_init();
+  }
+  if (warp == 1) sm100::tmem_alloc(&tmem_holder, 256);
+  // padding token rows [M, NT) of the codes, and all scale atoms, start at zero
+  for (int i = threadIdx.x; i < nkb * C::kSfStage / 16; i += kDecThreads)
+    reinterpret_cast<uint4*>(xsf)[i] = make_uint4(0, 0, 0, 0);
+  for (int i = threadIdx.x; i < nkb * (NT - g.M) * 8; i += kDecThreads) {
+    const int kb = i / ((NT - g.M) * 8), rest = i - kb * ((NT - g.M) * 8);
+    reinterpret_cast<uint4*>(xs + kb * xstage + (g.M + (rest >> 3)) * 128)[rest & 7] = make_uint4(0, 0, 0, 0);
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem_base = tmem_holder;
+
+  if (warp == 0) {
+    // ---- producer: whole weight tiles, 4-stage ring; the first stages before the PDL wait
+    if (lane == 0) {
+      int j = 0;
+      bool waited = false;
+      for (int t = blockIdx.x; t < g.row_tiles; t += gridDim.x)
+        for (int kb = 0; kb < nkb; ++kb, ++j) {
+          const int slot = j % kPStages;
+          if (j >= kPStages) {
+            if (!waited) { pdl_wait(); pdl_trigger(); waited = true; }
+            sm100::mbar_wait(&empty[slot], ((j / kPStages) & 1) ^ 1);
+          }
+          sm100::mbar_arrive_expect_tx(&full[slot], kDecStageCodes + C::kSfStage);
+          sm100::tma_load_2d(smem + C::kOffW + slot * kDecStageCodes, &tmW, &full[slot], kb * 128, t * 128);
+          sm100::bulk_load(smem + C::kOffWsf + slot * C::kSfStage,
+                           g.w_sf + ((int64_t)t * g.sf_col_blocks + (int64_t)kb * C::kAtoms) * 512, C::kSfStage,
+                           &full[slot]);
+        }
+      if (!waited) { pdl_wait(); pdl_trigger(); }
+    }
+    __syncwarp();
+  } else {
+    pdl_wait();
+    // ---- all of X -> SMEM operand (rotate + quantize; NVFP4: max pass first)
+    const int spr = nkb * 8, nseg = g.M * spr;
+    const int qt = (int)threadIdx.x - 32;
+    auto load_rotate = [&](int sidx, u64 (&P)[kPairs]) {
+      const int r = sidx / spr, cs = sidx - r * spr;
+      const uint4* src = reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(g.x) + (int64_t)r * g.K +
+                                                        (int64_t)cs * kSeg);
+      uint4 v[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) v[c] = __ldg(src + c);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const uint32_t w[4] = {v[c].x, v[c].y, v[c].z, v[c].w};
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          if constexpr (IN == MRFP4_DT_BF16) {
+            P[4 * c + t] = pk(__uint_as_float(w[t] << 16), __uint_as_float(w[t] & 0xFFFF0000u));
+          } else {
+            const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[t]));
+            P[4 * c + t] = pk(f.x, f.y);
+          }
+        }
+      }
+      if constexpr (HK > 0) fwht<HK>(P, 0, g.qp.pm);
+    };
+    EncConsts k;
+    if constexpr (FMT == MRFP4_FMT_NVFP4) {
+      float m = 0.f;
+#pragma unroll 1
+      for (int sidx = qt; sidx < nseg; sidx += kQThreads) {
+        u64 P[kPairs];
+        load_rotate(sidx, P);
+        float a0, a1;
+        half_amax(P, a0, a1);
+        m = max3n(a0, a1, m);
+      }
+      uint32_t mb = __float_as_uint(m);
+      mb = mb > 0x7f800000u ? 0x7fc00000u : mb;
+      mb = __reduce_max_sync(0xffffffffu, mb);
+      if (lane == 0) wmax[warp] = mb;
+      asm volatile("bar.sync 1, %0;" ::"r"(kQThreads) : "memory");
+      if (threadIdx.x == 32) {
+        uint32_t x = 0;
+        for (int i = 1; i < kDecThreads / 32; ++i) x = max(x, wmax[i]);
+        sk = nv_consts_fast(g.qp, kPow2C, x);
+      }
+      asm volatile("bar.sync 1, %0;" ::"r"(kQThreads) : "memory");
+      k = sk;
+    } else {
+      k.st32 = g.qp.mx_ts;
+    }
+    uint32_t bad = 0;
+#pragma unroll 1
+    for (int sidx = qt; sidx < nseg; sidx += kQThreads) {
+      u64 P[kPairs];
+      load_rotate(sidx, P);
+      const int r = sidx / spr, cs = sidx - r * spr;
+      const int kb = cs >> 3, chunk = cs & 7;
+      float a0, a1;
+      half_amax(P, a0, a1);
+      GroupScale s0, s1;
+      uint32_t sfc;
+      if constexpr (FMT == MRFP4_FMT_NVFP4) {
+        s0 = nv_group_scale<true>(a0, g.qp, k.kenc, k.knv, k.st32, k.st64, k.zero_code, kPow2C);
+        s1 = nv_group_scale<true>(a1, g.qp, k.kenc, k.knv, k.st32, k.st64, k.zero_code, kPow2C);
+        if (__float_as_uint(a0) >= 0x7f800000u || __float_as_uint(a1) >= 0x7f800000u) bad |= MRFP4_STATUS_NONFINITE;
+        if (s0.code == 0 || s1.code == 0) bad |= MRFP4_STATUS_SCALE_UNDERFLOW;
+        sfc = s0.code | (s1.code << 8);
+      } else {
+        const float a = max3n(a0, a1, 0.f);
+        if (__float_as_uint(a) >= 0x7f800000u) bad |= MRFP4_STATUS_NONFINITE;
+        s0 = mx_group_scale(a, g.qp);
+        s1 = s0;
+        sfc = s0.code;
+      }
+      uint32_t w4[4];
+      quantize_seg<true>(P, s0, s1, k.st32, g.qp, w4, kPow2C);
+      *reinterpret_cast<uint4*>(xs + kb * xstage + r * 128 + ((chunk ^ (r & 7)) << 4)) =
+          make_uint4(w4[0], w4[1], w4[2], w4[3]);
+      uint8_t* sfst = xsf + kb * C::kSfStage;
+      const int col = FMT == MRFP4_FMT_NVFP4 ? 2 * chunk : chunk;
+      const int off = (col >> 2) * 512 + (r & 31) * 16 + ((r >> 5) & 3) * 4 + (col & 3);
+      if constexpr (FMT == MRFP4_FMT_NVFP4)
+        *reinterpret_cast<uint16_t*>(sfst + off) = (uint16_t)sfc;
+      else
+        sfst[off] = (uint8_t)sfc;
+    }
+    if (bad && g.status) atomicOr(g.status, bad);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic SMEM writes -> tcgen05 reads
+    sm100::tc_fence_before();
+    asm volatile("bar.sync 1, %0;" ::"r"(kQThreads) : "memory");
+    sm100::tc_fence_after();
+
+    if (warp == 1) {
+      // ---- MMA: W tile (A, 128 rows) x resident X (B, NT tokens), alternating accumulators
+      const uint32_t el = sm100::elect_lane();
+      const uint32_t idesc = sm100::idesc_fp4(128, NT, VEC == 32, 0, 0);
+      const uint64_t wdesc0 = sm100::smem_desc(sm100::smem_u32(smem + C::kOffW), 16, 1024, 2);
+      const uint64_t xdesc0 = sm100::smem_desc(sm100::smem_u32(xs), 16, 1024, 2);
+      int j = 0, i = 0;
+      for (int t = blockIdx.x; t < g.row_tiles; t += gridDim.x, ++i) {
+        const int b = i & 1;
+        sm100::mbar_wait(&tempty[b], ((i >> 1) & 1) ^ 1);
+        sm100::tc_fence_after();
+        const uint32_t acc = tmem_base + (uint32_t)(b * 32);
+        for (int kb = 0; kb < nkb; ++kb, ++j) {
+          const int slot = j % kPStages;
+          sm100::mbar_wait(&full[slot], (j / kPStages) & 1);
+          sm100::tc_fence_after();
+          const uint32_t sfa = tmem_base + C::kSfBase + slot * C::kSfCols, sfb = sfa + C::kAtoms * 4;
+          const uint32_t wsf = sm100::smem_u32(smem + C::kOffWsf + slot * C::kSfStage);
+          const uint32_t xsfa = sm100::smem_u32(xsf + kb * C::kSfStage);
+#pragma unroll
+          for (int a = 0; a < C::kAtoms; ++a) {
+            tc_cp_if(el, sfa + a * 4, sm100::smem_desc(wsf + a * 512, 0, 128, 0));
+            tc_cp_if(el, sfb + a * 4, sm100::smem_desc(xsfa + a * 512, 0, 128, 0));
+          }
+          const uint64_t wd = dadd(wdesc0, (uint32_t)(slot * (kDecStageCodes >> 4)));
+          const uint64_t xd = dadd(xdesc0, (uint32_t)(kb * (xstage >> 4)));
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const uint32_t atom = VEC == 16 ? kk : (kk >> 1);
+            const uint32_t sfid = VEC == 16 ? 0u : (uint32_t)(kk & 1) * 2u;
+            const uint32_t id = idesc | (sfid << 4) | (sfid << 29);
+            tc_mma_fp4_if(el, VEC, acc, dadd(wd, 2 * kk), dadd(xd, 2 * kk), id, (sfa + atom * 4) | (sfid << 30),
+                          (sfb + atom * 4) | (sfid << 30), (kb | kk) ? 1u : 0u);
+          }
+          tc_commit_if(&empty[slot], el);
+          __syncwarp();
+        }
+        tc_commit_if(&tfull[b], el);
+        __syncwarp();
+      }
+    } else if (warp >= 4 && warp < 8) {
+      // ---- epilogue: TMEM lane quadrant q = one weight row per thread, Y stored directly
+      const int q = warp & 3, nl = q * 32 + lane;
+      const float alpha = k.st32 * w_ts;
+      int i = 0;
+      for (int t = blockIdx.x; t < g.row_tiles; t += gridDim.x, ++i) {
+        const int b = i & 1;
+        sm100::mbar_wait(&tfull[b], (i >> 1) & 1);
+        sm100::tc_fence_after();
+        uint32_t r[32];
+        sm100::tmem_ld_32x32b_x32(tmem_base + (uint32_t)(b * 32) + ((uint32_t)(q * 32) << 16), r);
+        sm100::tmem_ld_wait();
+        sm100::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) sm100::mbar_arrive(&tempty[b]);
+        const int64_t n = (int64_t)t * 128 + nl;
+#pragma unroll
+        for (int m = 0; m < 32; ++m) {
+          if (m < g.M) {
+            const float v = __uint_as_float(r[m]) * alpha;
+            if (g.out_f32) static_cast<float*>(g.d)[(int64_t)m * g.ldd + n] = v;
+            else static_cast<__nv_bfloat16*>(g.d)[(int64_t)m * g.ldd + n] = __float2bfloat16_rn(v);
+          }
+        }
+      }
+    }
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc(tmem_base, 256);
+  }
+}
+
 }  // namespace
 
 // Cluster plan of the fused decode linear: splits (= cluster size, a power of 2 <= 8) large
@@ -444,6 +704,22 @@ bool decode_plan(int64_t M, int64_t N, int64_t K, int* splits, int* kb_per) {
 }
 
 size_t decode_workspace_bytes(int64_t, int64_t, int64_t) { return 0; }
+
+// Plan of the persistent (wide-weight) decode kernel: the whole quantized activation resident in
+// shared memory (sized for NVFP4's larger scale atoms), at least one full wave of tiles.
+// Every CTA quantizes all M x K activations before its first MMA (~0.14 us per 1K elements,
+// measured), so it pays off while that stays small next to the two-kernel path's cost:
+// M * K <= 32K always, <= 64K for weights up to 64M elements (Llama-3-8B up_proj at M = 16:
+// 25.1 vs 29.4 us; 70B up_proj: 35.0 vs 45.7 us at M = 1, 45.0 vs 42.5 us at M = 8).
+bool decode_p_plan(int64_t M, int64_t N, int64_t K, int* grid) {
+  if (M < 1 || M > 32 || K % 256 || K < 256 || N % 128) return false;
+  if (!(M * K <= (1 << 15) || (M * K <= (1 << 16) && N * K <= (int64_t(1) << 26)))) return false;
+  const int NT = M <= 16 ? 16 : 32, nkb = (int)(K / 256);
+  if (PCfg<16>::smem(nkb, NT) > 227 * 1024 - 2048) return false;
+  const int tiles = (int)(N / 128);
+  *grid = std::min(tiles, device_sms());
+  return true;
+}
 
 // One launcher per instantiation: its own per-device attribute cache (a shared generic lambda
 // would share one static between kernels of the same signature).
@@ -475,12 +751,29 @@ int launch_decode_kernel(const CUtensorMap& tm, const DecArgs& g, cudaStream_t s
   return cudaLaunchKernelEx(&cfg, k_linear_decode<IN, V, H>, tm, g) == cudaSuccess ? MRFP4_OK : MRFP4_ECUDA;
 }
 
+template <int IN, int V, int H>
+int launch_decode_p_kernel(const CUtensorMap& tm, const DecArgs& g, cudaStream_t s) {
+  static std::atomic<int> attr[kMaxDevices];
+  if (per_device_once(attr, [&] {
+        return cudaFuncSetAttribute(k_linear_decode_p<IN, V, H>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    227 * 1024 - 2048) == cudaSuccess
+                   ? 1
+                   : -1;
+      }) < 0)
+    return MRFP4_ECUDA;
+  const int smem = PCfg<V>::smem(g.num_kb, g.NT);
+  return launch_pdl(k_linear_decode_p<IN, V, H>, dim3(g.pgrid), dim3(kDecThreads), smem, s, false, tm, g) ==
+                 cudaSuccess
+             ? MRFP4_OK
+             : MRFP4_ECUDA;
+}
+
 // Returns MRFP4_EUNSUPPORTED when the shape is not a decode shape (the caller uses K1 + K2).
 int launch_linear_decode(const void* x, int x_dtype, int64_t M, int64_t K, int fmt, int hk, const uint8_t* w,
                          const uint8_t* w_sf, const float* w_ts, int64_t N, void* d, int d_dtype, int64_t ldd,
                          void* ws, size_t ws_bytes, uint32_t* status, cudaStream_t s) {
   if (M < 1 || M > 32 || K % 256 || K < 256 || N % 128 || (hk != 0 && hk != 16 && hk != 32) ||
-      (x_dtype != MRFP4_DT_BF16 && x_dtype != MRFP4_DT_F16) || M * K > (1 << 18))
+      (x_dtype != MRFP4_DT_BF16 && x_dtype != MRFP4_DT_F16))
     return MRFP4_EUNSUPPORTED;
 
   DecArgs g{};
@@ -502,7 +795,11 @@ int launch_linear_decode(const void* x, int x_dtype, int64_t M, int64_t K, int f
   g.sf_col_blocks = ceil_div(K / G, 4);
   g.row_tiles = (int)(N / 128);
   g.num_kb = (int)(K / 256);
-  if (!decode_plan(M, N, K, &g.splits, &g.kb_per)) return MRFP4_EUNSUPPORTED;
+  bool persistent = false;
+  if (M * K > (1 << 18) || !decode_plan(M, N, K, &g.splits, &g.kb_per)) {
+    if (!decode_p_plan(M, N, K, &g.pgrid)) return MRFP4_EUNSUPPORTED;
+    persistent = true;
+  }
   (void)ws;
   (void)ws_bytes;
   g.qp.c64 = hk ? 1.0 / std::sqrt((double)hk) : 1.0;
@@ -523,8 +820,9 @@ int launch_linear_decode(const void* x, int x_dtype, int64_t M, int64_t K, int f
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return MRFP4_ECUDA;
-#define MRFP4_DEC(IN, V, H) \
-  if (x_dtype == IN && G == V && hk == H) return launch_decode_kernel<IN, V, H>(tm, g, s);
+#define MRFP4_DEC(IN, V, H)                                                                                    \
+  if (x_dtype == IN && G == V && hk == H)                                                                        \
+    return persistent ? launch_decode_p_kernel<IN, V, H>(tm, g, s) : launch_decode_kernel<IN, V, H>(tm, g, s);
   MRFP4_DEC(MRFP4_DT_BF16, 16, 16) MRFP4_DEC(MRFP4_DT_BF16, 16, 32) MRFP4_DEC(MRFP4_DT_BF16, 16, 0)
   MRFP4_DEC(MRFP4_DT_BF16, 32, 16) MRFP4_DEC(MRFP4_DT_BF16, 32, 32) MRFP4_DEC(MRFP4_DT_BF16, 32, 0)
   MRFP4_DEC(MRFP4_DT_F16, 16, 16) MRFP4_DEC(MRFP4_DT_F16, 16, 32) MRFP4_DEC(MRFP4_DT_F16, 16, 0)

@@ -1,5 +1,5 @@
 """The one-kernel decode linear (mrfp4_linear_decode: act-quant inside the GEMM CTAs, weight on
-the 128-row MMA side) against the oracle's dequantize(Aq) @ dequantize(Wq).T (formats.py:424-442)
+the 128-row MMA side; K-split clusters, or persistent CTAs for weights wider than one wave) against the oracle's dequantize(Aq) @ dequantize(Wq).T (formats.py:424-442)
 and against the two-kernel path (K1 + K2) it replaces for M <= 32."""
 
 import numpy as np
@@ -32,7 +32,9 @@ def two_kernel(x, w, out_dtype):
 @pytest.mark.parametrize("fmt,k", [("nvfp4", 16), ("mxfp4", 32), ("nvfp4", 32), ("mxfp4", 16), ("nvfp4", 0),
                                    ("mxfp4", 0)])
 @pytest.mark.parametrize("M,K,N", [(16, 4096, 4096), (1, 4096, 1024), (7, 2048, 384), (32, 4096, 1024),
-                                   (24, 256, 128), (1, 16384, 512), (16, 1024, 16384)])
+                                   (24, 256, 128), (1, 16384, 512), (16, 1024, 16384),
+                                   # wider than one wave of clusters: the persistent variant
+                                   (4, 2048, 24576), (24, 1024, 20480), (16, 4096, 14336)])
 def test_decode_kernel_vs_oracle_and_two_kernel_path(fmt, k, M, K, N):
     rng = np.random.default_rng(M * 7 + K + N + k)
     X = O.bf16_round(rng.standard_normal((M, K)) * np.exp(rng.uniform(-1, 1, size=(M, 1))))
