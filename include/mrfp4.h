@@ -236,12 +236,15 @@ int mrfp4_mse_group_err(const double* y, int64_t ngroups, int fmt, const double*
  * weight on the 128-row MMA side (D^T = W . Xq^T, N = 16 | 32 tokens).  Same result as
  * mrfp4_act_quant + mrfp4_gemm up to fp32 summation order.  x: [M, K] contiguous bf16 / f16;
  * w: [N, K/2] codes + swizzled scales + device tensor scale; d: [M, N] (row stride ldd) bf16 /
- * f32.  One thread-block cluster per 128-row weight tile, its CTAs splitting K (<= 8): the
- * NVFP4 whole-tensor max and the K-split partial sums are combined over distributed shared
- * memory, so no workspace and no grid-wide synchronization is involved.  Requires K % 256 == 0,
- * N % 128 == 0, had_k in {0, 16, 32}, M * K <= 2^18 and a slice of <= 16K elements per CTA;
- * returns MRFP4_EUNSUPPORTED otherwise (use mrfp4_act_quant + mrfp4_gemm).  workspace: unused
- * (mrfp4_linear_decode_workspace() returns 0).  status: optional device word for the DataError bits.
+ * f32.  Two variants, chosen by shape: one thread-block cluster per 128-row weight tile, its
+ * CTAs splitting K (<= 8) with the NVFP4 whole-tensor max and the K-split partial sums combined
+ * over distributed shared memory (when row tiles x splits fit one wave); or, for wider weights
+ * with small M * K, persistent CTAs that each quantize the whole activation into shared memory
+ * and stream whole weight tiles.  No workspace, no grid-wide synchronization.  Requires
+ * K % 256 == 0, N % 128 == 0, had_k in {0, 16, 32}; returns MRFP4_EUNSUPPORTED for shapes
+ * neither variant takes (use mrfp4_act_quant + mrfp4_gemm; mrfp4_linear_decode_ctas() == 0).
+ * workspace: unused (mrfp4_linear_decode_workspace() returns 0).  status: optional device word for
+ * the DataError bits.
  */
 size_t mrfp4_linear_decode_workspace(int64_t M, int64_t N, int64_t K);
 /* CTAs mrfp4_linear_decode launches for this shape (0: not a decode shape it takes). */
