@@ -438,6 +438,7 @@ __global__ void __launch_bounds__(kDecThreads, 1)
 // epilogue (direct Y stores) overlaps the next tile's MMAs.  The weight prefetch starts before
 // the PDL wait and runs under the activation quantization.
 constexpr int kPStages = 4;
+constexpr int kPMaxChunks = 64;
 
 template <int VEC>
 struct PCfg {
@@ -457,10 +458,10 @@ __global__ void __launch_bounds__(kDecThreads, 1)
   using C = PCfg<VEC>;
   constexpr int FMT = VEC == 16 ? MRFP4_FMT_NVFP4 : MRFP4_FMT_MXFP4;
   constexpr bool kPow2C = HK == 0 || HK == 16;
-  constexpr int kQThreads = kDecThreads - 32;   // warps 1.. quantize X; warp 0 is the producer
+  constexpr int kQThreads = kDecThreads - 64;   // warps 2..15 quantize X (0: producer, 1: MMA)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ __align__(8) uint64_t full[kPStages], empty[kPStages], tfull[2], tempty[2];
+  __shared__ __align__(8) uint64_t full[kPStages], empty[kPStages], tfull[2], tempty[2], xready[kPMaxChunks];
   __shared__ uint32_t tmem_holder, wmax[kDecThreads / 32];
   __shared__ EncConsts sk;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -469,6 +470,8 @@ __global__ void __launch_bounds__(kDecThreads, 1)
   uint8_t* const xs = smem + C::kOffX;
   uint8_t* const xsf = xs + nkb * xstage;
   const float w_ts = __ldg(g.w_ts);
+  // activation chunks of ck k-blocks (about one segment per quantizing thread each)
+  const int ck = max(1, min(nkb, (2 * kQThreads) / (g.M * 8))), nchunks = (nkb + ck - 1) / ck;
 
   if (warp == 0 && lane == 0) {
     sm100::tma_prefetch_desc(&tmW);
@@ -480,6 +483,7 @@ __global__ void __launch_bounds__(kDecThreads, 1)
       sm100::mbar_init(&tfull[i], 1);
       sm100::mbar_init(&tempty[i], 4);
     }
+    for (int i = 0; i < nchunks; ++i) sm100::mbar_init(&xready[i], kQThreads);
     sm100::fence_mbar_init();
   }
   if (warp == 1) sm100::tmem_alloc(&tmem_holder, 256);
@@ -516,13 +520,58 @@ __global__ void __launch_bounds__(kDecThreads, 1)
       if (!waited) { pdl_wait(); pdl_trigger(); }
     }
     __syncwarp();
+  } else if (warp == 1) {
+    // ---- MMA: W tile (A, 128 rows) x resident X (B, NT tokens), alternating accumulators; in
+    // the first tile each activation chunk is waited for as it is quantized (xready)
+    const uint32_t el = sm100::elect_lane();
+    const uint32_t idesc = sm100::idesc_fp4(128, NT, VEC == 32, 0, 0);
+    const uint64_t wdesc0 = sm100::smem_desc(sm100::smem_u32(smem + C::kOffW), 16, 1024, 2);
+    const uint64_t xdesc0 = sm100::smem_desc(sm100::smem_u32(xs), 16, 1024, 2);
+    int j = 0, i = 0, xr = 0;
+    for (int t = blockIdx.x; t < g.row_tiles; t += gridDim.x, ++i) {
+      const int b = i & 1;
+      sm100::mbar_wait(&tempty[b], ((i >> 1) & 1) ^ 1);
+      sm100::tc_fence_after();
+      const uint32_t acc = tmem_base + (uint32_t)(b * 32);
+      for (int kb = 0; kb < nkb; ++kb, ++j) {
+        if (kb >= xr * ck) {
+          sm100::mbar_wait(&xready[xr], 0);
+          ++xr;
+        }
+        const int slot = j % kPStages;
+        sm100::mbar_wait(&full[slot], (j / kPStages) & 1);
+        sm100::tc_fence_after();
+        const uint32_t sfa = tmem_base + C::kSfBase + slot * C::kSfCols, sfb = sfa + C::kAtoms * 4;
+        const uint32_t wsf = sm100::smem_u32(smem + C::kOffWsf + slot * C::kSfStage);
+        const uint32_t xsfa = sm100::smem_u32(xsf + kb * C::kSfStage);
+#pragma unroll
+        for (int a = 0; a < C::kAtoms; ++a) {
+          tc_cp_if(el, sfa + a * 4, sm100::smem_desc(wsf + a * 512, 0, 128, 0));
+          tc_cp_if(el, sfb + a * 4, sm100::smem_desc(xsfa + a * 512, 0, 128, 0));
+        }
+        const uint64_t wd = dadd(wdesc0, (uint32_t)(slot * (kDecStageCodes >> 4)));
+        const uint64_t xd = dadd(xdesc0, (uint32_t)(kb * (xstage >> 4)));
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const uint32_t atom = VEC == 16 ? kk : (kk >> 1);
+          const uint32_t sfid = VEC == 16 ? 0u : (uint32_t)(kk & 1) * 2u;
+          const uint32_t id = idesc | (sfid << 4) | (sfid << 29);
+          tc_mma_fp4_if(el, VEC, acc, dadd(wd, 2 * kk), dadd(xd, 2 * kk), id, (sfa + atom * 4) | (sfid << 30),
+                        (sfb + atom * 4) | (sfid << 30), (kb | kk) ? 1u : 0u);
+        }
+        tc_commit_if(&empty[slot], el);
+        __syncwarp();
+      }
+      tc_commit_if(&tfull[b], el);
+      __syncwarp();
+    }
   } else {
     pdl_wait();
-    // ---- all of X -> SMEM operand (rotate + quantize; NVFP4: max pass first)
+    // ---- warps 2..15: all of X -> SMEM operand (rotate + quantize; NVFP4: max pass first), in
+    // chunks of ck k-blocks, each announced to the MMA warp (xready) as soon as it is written
     const int spr = nkb * 8, nseg = g.M * spr;
-    const int qt = (int)threadIdx.x - 32;
-    auto load_rotate = [&](int sidx, u64 (&P)[kPairs]) {
-      const int r = sidx / spr, cs = sidx - r * spr;
+    const int qt = (int)threadIdx.x - 64;
+    auto load_rotate = [&](int r, int cs, u64 (&P)[kPairs]) {
       const uint4* src = reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(g.x) + (int64_t)r * g.K +
                                                         (int64_t)cs * kSeg);
       uint4 v[4];
@@ -549,7 +598,8 @@ __global__ void __launch_bounds__(kDecThreads, 1)
 #pragma unroll 1
       for (int sidx = qt; sidx < nseg; sidx += kQThreads) {
         u64 P[kPairs];
-        load_rotate(sidx, P);
+        const int r = sidx / spr;
+        load_rotate(r, sidx - r * spr, P);
         float a0, a1;
         half_amax(P, a0, a1);
         m = max3n(a0, a1, m);
@@ -559,9 +609,9 @@ __global__ void __launch_bounds__(kDecThreads, 1)
       mb = __reduce_max_sync(0xffffffffu, mb);
       if (lane == 0) wmax[warp] = mb;
       asm volatile("bar.sync 1, %0;" ::"r"(kQThreads) : "memory");
-      if (threadIdx.x == 32) {
+      if (threadIdx.x == 64) {
         uint32_t x = 0;
-        for (int i = 1; i < kDecThreads / 32; ++i) x = max(x, wmax[i]);
+        for (int i = 2; i < kDecThreads / 32; ++i) x = max(x, wmax[i]);
         sk = nv_consts_fast(g.qp, kPow2C, x);
       }
       asm volatile("bar.sync 1, %0;" ::"r"(kQThreads) : "memory");
@@ -570,88 +620,51 @@ __global__ void __launch_bounds__(kDecThreads, 1)
       k.st32 = g.qp.mx_ts;
     }
     uint32_t bad = 0;
+    const int per_chunk = g.M * 8 * ck;                 // segments of one chunk, k-block major
+    for (int c = 0; c < nchunks; ++c) {
+      const int kb0c = c * ck, nsc = min(per_chunk, nseg - kb0c * g.M * 8);
 #pragma unroll 1
-    for (int sidx = qt; sidx < nseg; sidx += kQThreads) {
-      u64 P[kPairs];
-      load_rotate(sidx, P);
-      const int r = sidx / spr, cs = sidx - r * spr;
-      const int kb = cs >> 3, chunk = cs & 7;
-      float a0, a1;
-      half_amax(P, a0, a1);
-      GroupScale s0, s1;
-      uint32_t sfc;
-      if constexpr (FMT == MRFP4_FMT_NVFP4) {
-        s0 = nv_group_scale<true>(a0, g.qp, k.kenc, k.knv, k.st32, k.st64, k.zero_code, kPow2C);
-        s1 = nv_group_scale<true>(a1, g.qp, k.kenc, k.knv, k.st32, k.st64, k.zero_code, kPow2C);
-        if (__float_as_uint(a0) >= 0x7f800000u || __float_as_uint(a1) >= 0x7f800000u) bad |= MRFP4_STATUS_NONFINITE;
-        if (s0.code == 0 || s1.code == 0) bad |= MRFP4_STATUS_SCALE_UNDERFLOW;
-        sfc = s0.code | (s1.code << 8);
-      } else {
-        const float a = max3n(a0, a1, 0.f);
-        if (__float_as_uint(a) >= 0x7f800000u) bad |= MRFP4_STATUS_NONFINITE;
-        s0 = mx_group_scale(a, g.qp);
-        s1 = s0;
-        sfc = s0.code;
+      for (int e = qt; e < nsc; e += kQThreads) {
+        const int kbl = e / (g.M * 8), rem = e - kbl * (g.M * 8);
+        const int r = rem >> 3, chunk = rem & 7, kb = kb0c + kbl;
+        u64 P[kPairs];
+        load_rotate(r, kb * 8 + chunk, P);
+        float a0, a1;
+        half_amax(P, a0, a1);
+        GroupScale s0, s1;
+        uint32_t sfc;
+        if constexpr (FMT == MRFP4_FMT_NVFP4) {
+          s0 = nv_group_scale<true>(a0, g.qp, k.kenc, k.knv, k.st32, k.st64, k.zero_code, kPow2C);
+          s1 = nv_group_scale<true>(a1, g.qp, k.kenc, k.knv, k.st32, k.st64, k.zero_code, kPow2C);
+          if (__float_as_uint(a0) >= 0x7f800000u || __float_as_uint(a1) >= 0x7f800000u)
+            bad |= MRFP4_STATUS_NONFINITE;
+          if (s0.code == 0 || s1.code == 0) bad |= MRFP4_STATUS_SCALE_UNDERFLOW;
+          sfc = s0.code | (s1.code << 8);
+        } else {
+          const float a = max3n(a0, a1, 0.f);
+          if (__float_as_uint(a) >= 0x7f800000u) bad |= MRFP4_STATUS_NONFINITE;
+          s0 = mx_group_scale(a, g.qp);
+          s1 = s0;
+          sfc = s0.code;
+        }
+        uint32_t w4[4];
+        quantize_seg<true>(P, s0, s1, k.st32, g.qp, w4, kPow2C);
+        *reinterpret_cast<uint4*>(xs + kb * xstage + r * 128 + ((chunk ^ (r & 7)) << 4)) =
+            make_uint4(w4[0], w4[1], w4[2], w4[3]);
+        uint8_t* sfst = xsf + kb * C::kSfStage;
+        const int col = FMT == MRFP4_FMT_NVFP4 ? 2 * chunk : chunk;
+        const int off = (col >> 2) * 512 + (r & 31) * 16 + ((r >> 5) & 3) * 4 + (col & 3);
+        if constexpr (FMT == MRFP4_FMT_NVFP4)
+          *reinterpret_cast<uint16_t*>(sfst + off) = (uint16_t)sfc;
+        else
+          sfst[off] = (uint8_t)sfc;
       }
-      uint32_t w4[4];
-      quantize_seg<true>(P, s0, s1, k.st32, g.qp, w4, kPow2C);
-      *reinterpret_cast<uint4*>(xs + kb * xstage + r * 128 + ((chunk ^ (r & 7)) << 4)) =
-          make_uint4(w4[0], w4[1], w4[2], w4[3]);
-      uint8_t* sfst = xsf + kb * C::kSfStage;
-      const int col = FMT == MRFP4_FMT_NVFP4 ? 2 * chunk : chunk;
-      const int off = (col >> 2) * 512 + (r & 31) * 16 + ((r >> 5) & 3) * 4 + (col & 3);
-      if constexpr (FMT == MRFP4_FMT_NVFP4)
-        *reinterpret_cast<uint16_t*>(sfst + off) = (uint16_t)sfc;
-      else
-        sfst[off] = (uint8_t)sfc;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // this thread's writes -> tcgen05
+      sm100::mbar_arrive(&xready[c]);
     }
     if (bad && g.status) atomicOr(g.status, bad);
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic SMEM writes -> tcgen05 reads
-    sm100::tc_fence_before();
-    asm volatile("bar.sync 1, %0;" ::"r"(kQThreads) : "memory");
-    sm100::tc_fence_after();
 
-    if (warp == 1) {
-      // ---- MMA: W tile (A, 128 rows) x resident X (B, NT tokens), alternating accumulators
-      const uint32_t el = sm100::elect_lane();
-      const uint32_t idesc = sm100::idesc_fp4(128, NT, VEC == 32, 0, 0);
-      const uint64_t wdesc0 = sm100::smem_desc(sm100::smem_u32(smem + C::kOffW), 16, 1024, 2);
-      const uint64_t xdesc0 = sm100::smem_desc(sm100::smem_u32(xs), 16, 1024, 2);
-      int j = 0, i = 0;
-      for (int t = blockIdx.x; t < g.row_tiles; t += gridDim.x, ++i) {
-        const int b = i & 1;
-        sm100::mbar_wait(&tempty[b], ((i >> 1) & 1) ^ 1);
-        sm100::tc_fence_after();
-        const uint32_t acc = tmem_base + (uint32_t)(b * 32);
-        for (int kb = 0; kb < nkb; ++kb, ++j) {
-          const int slot = j % kPStages;
-          sm100::mbar_wait(&full[slot], (j / kPStages) & 1);
-          sm100::tc_fence_after();
-          const uint32_t sfa = tmem_base + C::kSfBase + slot * C::kSfCols, sfb = sfa + C::kAtoms * 4;
-          const uint32_t wsf = sm100::smem_u32(smem + C::kOffWsf + slot * C::kSfStage);
-          const uint32_t xsfa = sm100::smem_u32(xsf + kb * C::kSfStage);
-#pragma unroll
-          for (int a = 0; a < C::kAtoms; ++a) {
-            tc_cp_if(el, sfa + a * 4, sm100::smem_desc(wsf + a * 512, 0, 128, 0));
-            tc_cp_if(el, sfb + a * 4, sm100::smem_desc(xsfa + a * 512, 0, 128, 0));
-          }
-          const uint64_t wd = dadd(wdesc0, (uint32_t)(slot * (kDecStageCodes >> 4)));
-          const uint64_t xd = dadd(xdesc0, (uint32_t)(kb * (xstage >> 4)));
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            const uint32_t atom = VEC == 16 ? kk : (kk >> 1);
-            const uint32_t sfid = VEC == 16 ? 0u : (uint32_t)(kk & 1) * 2u;
-            const uint32_t id = idesc | (sfid << 4) | (sfid << 29);
-            tc_mma_fp4_if(el, VEC, acc, dadd(wd, 2 * kk), dadd(xd, 2 * kk), id, (sfa + atom * 4) | (sfid << 30),
-                          (sfb + atom * 4) | (sfid << 30), (kb | kk) ? 1u : 0u);
-          }
-          tc_commit_if(&empty[slot], el);
-          __syncwarp();
-        }
-        tc_commit_if(&tfull[b], el);
-        __syncwarp();
-      }
-    } else if (warp >= 4 && warp < 8) {
+    if (warp >= 4 && warp < 8) {
       // ---- epilogue: TMEM lane quadrant q = one weight row per thread, Y stored directly
       const int q = warp & 3, nl = q * 32 + lane;
       const float alpha = k.st32 * w_ts;
@@ -713,7 +726,10 @@ size_t decode_workspace_bytes(int64_t, int64_t, int64_t) { return 0; }
 // 25.1 vs 29.4 us; 70B up_proj: 35.0 vs 45.7 us at M = 1, 45.0 vs 42.5 us at M = 8).
 bool decode_p_plan(int64_t M, int64_t N, int64_t K, int* grid) {
   if (M < 1 || M > 32 || K % 256 || K < 256 || N % 128) return false;
-  if (!(M * K <= (1 << 15) || (M * K <= (1 << 16) && N * K <= (int64_t(1) << 26)))) return false;
+#ifndef MRFP4_DECP_MK
+#define MRFP4_DECP_MK (1 << 15)
+#endif
+  if (!(M * K <= MRFP4_DECP_MK || (M * K <= (1 << 16) && N * K <= (int64_t(1) << 26)))) return false;
   const int NT = M <= 16 ? 16 : 32, nkb = (int)(K / 256);
   if (PCfg<16>::smem(nkb, NT) > 227 * 1024 - 2048) return false;
   const int tiles = (int)(N / 128);
