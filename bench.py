@@ -114,6 +114,22 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
+class stdout_to_stderr:
+    """Route file descriptor 1 to 2 for a block (C-level library prints included)."""
+
+    def __enter__(self):
+        sys.stdout.flush()
+        self.saved = os.dup(1)
+        os.dup2(2, 1)
+        return self
+
+    def __exit__(self, *exc):
+        sys.stdout.flush()
+        os.dup2(self.saved, 1)
+        os.close(self.saved)
+        return False
+
+
 # ----------------------------------------------------------------------------- CPU arms
 def load_reference():
     """The stock reference package staged into oracle/_ref by oracle/make_ref.py, or None."""
@@ -469,7 +485,8 @@ def main():
             sys.path.insert(0, os.path.join(ROOT, "scripts"))
             import fp4_comparators
             act_quant_into(x, w.fmt, had, a.codes, a.sf, a.tensor_scale_dev, a.scratch)
-            comparators = fp4_comparators.run(x, a, w, fmt, had, flush_l2)
+            with stdout_to_stderr():   # libraries print to fd 1; the bench prints ONE JSON line
+                comparators = fp4_comparators.run(x, a, w, fmt, had, flush_l2)
             comparators["ours_k2"] = {"us": k2_mean * 1e6, "tflops": k2_flops / k2_mean / 1e12}
             comparators["ours_k1"] = {"us": k1_mean * 1e6, "gbs": k1_bytes / k1_mean / 1e9}
         except Exception as e:  # noqa: BLE001 - optional context
