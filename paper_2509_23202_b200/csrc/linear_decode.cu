@@ -731,7 +731,7 @@ bool decode_p_plan(int64_t M, int64_t N, int64_t K, int* grid) {
 #endif
   if (!(M * K <= MRFP4_DECP_MK || (M * K <= (1 << 16) && N * K <= (int64_t(1) << 26)))) return false;
   const int NT = M <= 16 ? 16 : 32, nkb = (int)(K / 256);
-  if (PCfg<16>::smem(nkb, NT) > 227 * 1024 - 2048) return false;
+  if (PCfg<16>::smem(nkb, NT) > 227 * 1024 - 2048 || nkb > kPMaxChunks) return false;
   const int tiles = (int)(N / 128);
   *grid = std::min(tiles, device_sms());
   return true;
