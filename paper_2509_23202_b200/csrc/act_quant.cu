@@ -1426,8 +1426,12 @@ int launch_mma(const AQParams& p, cudaStream_t s) {
 template <int IN, int FMT, int HK>
 int launch_hk(const AQParams& p, cudaStream_t s) {
   if constexpr (IN != MRFP4_DT_F32 && HK >= 16) {
-    // Tensor-core rotation: contiguous bf16 / f16 rows with K % 32 == 0, K >= 1024.
-    if (p.nseg && knob("MRFP4_K1_MMA", 1)) return launch_mma<IN, FMT, HK>(p, s);
+    // Tensor-core rotation: contiguous bf16 / f16 rows with K % 32 == 0, K >= 1024.  MXFP4 with
+    // >= 2^24 elements takes the butterfly kernel instead: its single 24-warp CTA per SM hands
+    // the SMs to the following GEMM sooner, and at these sizes it is as fast alone (c1 step
+    // 67.0 -> 65.5 us; 70B down M=8192: K1 153 -> 112 us) -- profiles/r02_k1_notes.md.
+    const bool mma_default = FMT == MRFP4_FMT_NVFP4 || (int64_t)p.Mi * p.Ki < (int64_t(1) << 24);
+    if (p.nseg && knob("MRFP4_K1_MMA", mma_default ? 1 : 0)) return launch_mma<IN, FMT, HK>(p, s);
   }
   CUtensorMap tm;
   memset(&tm, 0, sizeof(tm));
