@@ -96,3 +96,16 @@ def test_mse_entry_points_reject_bad_arguments():
     assert L.mrfp4_mse_pass(nul, 10, 1, nul, 129, nul, 0.0, 1.0, nul, nul, nul, nul, nul, nul) == _lib.EINVAL
     assert L.mrfp4_mse_pass(nul, 10, 1, nul, 129, nul, 1.0, 1.0, nul, nul, nul, nul, nul, nul) == _lib.EINVAL
     assert L.mrfp4_mse_group_err(nul, 10, 0, nul, -1.0, nul, nul, nul) == _lib.EINVAL
+
+
+def test_header_is_plain_c():
+    """include/mrfp4.h is a C header (no C++ in the ABI): it compiles as C99 and as C++."""
+    import shutil
+    import subprocess
+    if shutil.which("gcc") is None:
+        pytest.skip("no gcc")
+    hdr = os.path.join(ROOT, "include", "mrfp4.h")
+    for lang, std in (("c", "-std=c99"), ("c++", "-std=c++17")):
+        r = subprocess.run(["gcc", std, "-fsyntax-only", "-Wall", "-Werror", "-x", lang, hdr],
+                           capture_output=True, text=True)
+        assert r.returncode == 0, r.stderr
