@@ -299,9 +299,9 @@ def main():
     if "fused" in gathers:
         try:
             po = PeerOutputs(M, N, device=dev)
-        except Exception as e:  # symmetric memory unavailable: NCCL only
+        except Exception as e:  # symmetric memory unavailable: decided collectively below
             print(f"fused gather unavailable: {e!r}", file=sys.stderr)
-            gathers = [gg for gg in gathers if gg != "fused"] or ["nccl"]
+            po = None
     cols = slice(rank * w.N, (rank + 1) * w.N)
 
     # Decode-sized layers (M <= 32) run as ONE kernel: the act-quant inside the GEMM CTAs
@@ -315,11 +315,12 @@ def main():
     def step_nccl():
         if fused_decode:
             _linear_decode(x, w, y, dws, None)
-            return
+            return y
         act_quant_into(x, w.fmt, had, a.codes, a.sf, a.tensor_scale_dev, a.scratch)
         P.gemm(a, w, y)
         if sharded:
-            gather_columns(y, None)
+            return gather_columns(y, None)
+        return y
 
     def step_fused():
         act_quant_into(x, w.fmt, had, a.codes, a.sf, a.tensor_scale_dev, a.scratch)
@@ -328,6 +329,25 @@ def main():
         po.barrier(1)
 
     step = step_nccl
+
+    # The fused gather is checked against the NCCL one on this node before it is timed, and the
+    # decision to keep it is collective (a rank that would skip it alone would hang the others).
+    if sharded and "fused" in gathers:
+        ok = po is not None
+        if ok:
+            try:
+                ref = step_nccl().clone()
+                step_fused()
+                torch.cuda.synchronize(dev)
+                ok = bool(torch.equal(po.local, ref))
+            except Exception as e:  # noqa: BLE001
+                print(f"fused gather failed its check: {e!r}", file=sys.stderr)
+                ok = False
+        flag = torch.tensor([1 if ok else 0], device=dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if not int(flag.item()):
+            print("fused gather disabled on every rank (unavailable or mismatching)", file=sys.stderr)
+            gathers = [gg for gg in gathers if gg != "fused"] or ["nccl"]
 
     def barrier():
         if sharded:
