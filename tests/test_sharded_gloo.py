@@ -6,7 +6,9 @@ each rank owns rows [r*N/P, (r+1)*N/P) of the prepared weight, computes its
 without a GPU, that (1) ``PackedWeight.shard`` slices codes and the swizzled
 scale-factor atoms so every shard is a self-consistent weight of N/P rows, and
 (2) ``gather_columns`` reassembles the per-rank blocks into exactly the
-unsharded oracle output (dequantize(A) @ dequantize(W).T, formats.py:424-442).
+unsharded oracle output (dequantize(A) @ dequantize(W).T, formats.py:424-442), and (3)
+``quantized_linear_sharded``'s host flow reproduces it with the per-rank GPU linear replaced by
+the oracle's block (the GPU path itself: tests/test_gpu_multi.py).
 """
 
 import os
@@ -66,6 +68,23 @@ def _worker(rank: int, world: int, port: int, fmt_name: str, q):
         y = gather_columns(y_blk, None)
         assert y.shape == (M, N)
         assert np.array_equal(y.numpy(), y_full)
+        # (3) quantized_linear_sharded's host flow (leading dims, per-rank block, gather, reshape)
+        # with the per-rank GPU linear replaced, for this CPU test only, by the oracle's block
+        import paper_2509_23202_b200.sharded as S
+
+        def block_linear(x, w_shard, out_dtype=torch.bfloat16):
+            assert w_shard.N == hi - lo and tuple(x.shape[-1:]) == (K,)
+            return torch.from_numpy(np.ascontiguousarray(y_full[:, lo:hi])).reshape(*x.shape[:-1], hi - lo)
+
+        real = S.quantized_linear
+        S.quantized_linear = block_linear
+        try:
+            x3 = torch.from_numpy(X.astype(np.float32)).reshape(2, M // 2, K)
+            y3 = S.quantized_linear_sharded(x3, sh)
+        finally:
+            S.quantized_linear = real
+        assert tuple(y3.shape) == (2, M // 2, N)
+        assert np.array_equal(y3.reshape(M, N).numpy(), y_full)
         dist.destroy_process_group()
         q.put((rank, "ok"))
     except Exception as e:  # pragma: no cover - reported to the parent
