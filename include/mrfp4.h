@@ -241,7 +241,7 @@ int mrfp4_mse_group_err(const double* y, int64_t ngroups, int fmt, const double*
  * over distributed shared memory (when row tiles x splits fit one wave); or, for wider weights
  * with small M * K, persistent CTAs that each quantize the whole activation into shared memory
  * and stream whole weight tiles.  No workspace, no grid-wide synchronization.  Requires
- * K % 256 == 0, N % 128 == 0, had_k in {0, 16, 32}; returns MRFP4_EUNSUPPORTED for shapes
+ * K % 256 == 0, N % 128 == 0, had_k in {0, 16, 32, 64, 128}; returns MRFP4_EUNSUPPORTED for shapes
  * neither variant takes (use mrfp4_act_quant + mrfp4_gemm; mrfp4_linear_decode_ctas() == 0).
  * workspace: unused (mrfp4_linear_decode_workspace() returns 0).  status: optional device word for
  * the DataError bits.

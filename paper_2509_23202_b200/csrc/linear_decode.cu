@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(kDecThreads, 1)
     k_linear_decode(const __grid_constant__ CUtensorMap tmW, DecArgs g) {
   using C = DecCfg<VEC>;
   constexpr int FMT = VEC == 16 ? MRFP4_FMT_NVFP4 : MRFP4_FMT_MXFP4;
-  constexpr bool kPow2C = HK == 0 || HK == 16;   // c64 = 1 / sqrt(k) a power of 2
+  constexpr bool kPow2C = HK == 0 || HK == 16 || HK == 64;   // c64 = 1 / sqrt(k) a power of 2
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ __align__(8) uint64_t full[kDecStages], empty[kDecStages], tfull, mbar_max, mbar_part;
@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(kDecThreads, 1)
           }
         }
       }
-      if constexpr (HK > 0) fwht<HK>(P[b], 0, g.qp.pm);
+      if constexpr (HK > 0) fwht<HK>(P[b], lane, g.qp.pm);   // k = 64 / 128: partners in lane ^ 1, ^ 2
     }
   }
   stamp(6);
@@ -457,7 +457,7 @@ __global__ void __launch_bounds__(kDecThreads, 1)
     k_linear_decode_p(const __grid_constant__ CUtensorMap tmW, DecArgs g) {
   using C = PCfg<VEC>;
   constexpr int FMT = VEC == 16 ? MRFP4_FMT_NVFP4 : MRFP4_FMT_MXFP4;
-  constexpr bool kPow2C = HK == 0 || HK == 16;
+  constexpr bool kPow2C = HK == 0 || HK == 16 || HK == 64;
   constexpr int kQThreads = kDecThreads - 64;   // warps 2..15 quantize X (0: producer, 1: MMA)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -571,12 +571,15 @@ __global__ void __launch_bounds__(kDecThreads, 1)
     // chunks of ck k-blocks, each announced to the MMA warp (xready) as soon as it is written
     const int spr = nkb * 8, nseg = g.M * spr;
     const int qt = (int)threadIdx.x - 64;
-    auto load_rotate = [&](int r, int cs, u64 (&P)[kPairs]) {
+    // Loops run the same trip count in every lane (lanes past the end rotate zeros): the k = 64 /
+    // 128 butterfly stages exchange with lane ^ 1 / ^ 2, which hold the row's neighbouring segments
+    // (segment index = lane mod 32; 448 threads, rows and chunks of 8 segments).
+    auto load_rotate = [&](int r, int cs, bool valid, u64 (&P)[kPairs]) {
       const uint4* src = reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(g.x) + (int64_t)r * g.K +
                                                         (int64_t)cs * kSeg);
       uint4 v[4];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) v[c] = __ldg(src + c);
+      for (int c = 0; c < 4; ++c) v[c] = valid ? __ldg(src + c) : make_uint4(0, 0, 0, 0);
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         const uint32_t w[4] = {v[c].x, v[c].y, v[c].z, v[c].w};
@@ -590,16 +593,18 @@ __global__ void __launch_bounds__(kDecThreads, 1)
           }
         }
       }
-      if constexpr (HK > 0) fwht<HK>(P, 0, g.qp.pm);
+      if constexpr (HK > 0) fwht<HK>(P, lane, g.qp.pm);
     };
     EncConsts k;
     if constexpr (FMT == MRFP4_FMT_NVFP4) {
       float m = 0.f;
 #pragma unroll 1
-      for (int sidx = qt; sidx < nseg; sidx += kQThreads) {
+      for (int base = 0; base < nseg; base += kQThreads) {
+        const int sidx = base + qt;
+        const bool valid = sidx < nseg;
         u64 P[kPairs];
-        const int r = sidx / spr;
-        load_rotate(r, sidx - r * spr, P);
+        const int r = valid ? sidx / spr : 0;
+        load_rotate(r, valid ? sidx - r * spr : 0, valid, P);
         float a0, a1;
         half_amax(P, a0, a1);
         m = max3n(a0, a1, m);
@@ -624,11 +629,15 @@ __global__ void __launch_bounds__(kDecThreads, 1)
     for (int c = 0; c < nchunks; ++c) {
       const int kb0c = c * ck, nsc = min(per_chunk, nseg - kb0c * g.M * 8);
 #pragma unroll 1
-      for (int e = qt; e < nsc; e += kQThreads) {
+      for (int base = 0; base < nsc; base += kQThreads) {
+        const int e0 = base + qt;
+        const bool valid = e0 < nsc;
+        const int e = valid ? e0 : 0;
         const int kbl = e / (g.M * 8), rem = e - kbl * (g.M * 8);
         const int r = rem >> 3, chunk = rem & 7, kb = kb0c + kbl;
         u64 P[kPairs];
-        load_rotate(r, kb * 8 + chunk, P);
+        load_rotate(r, kb * 8 + chunk, valid, P);
+        if (!valid) continue;   // after the (lane-exchanging) rotation
         float a0, a1;
         half_amax(P, a0, a1);
         GroupScale s0, s1;
@@ -788,7 +797,7 @@ int launch_decode_p_kernel(const CUtensorMap& tm, const DecArgs& g, cudaStream_t
 int launch_linear_decode(const void* x, int x_dtype, int64_t M, int64_t K, int fmt, int hk, const uint8_t* w,
                          const uint8_t* w_sf, const float* w_ts, int64_t N, void* d, int d_dtype, int64_t ldd,
                          void* ws, size_t ws_bytes, uint32_t* status, cudaStream_t s) {
-  if (M < 1 || M > 32 || K % 256 || K < 256 || N % 128 || (hk != 0 && hk != 16 && hk != 32) ||
+  if (M < 1 || M > 32 || K % 256 || K < 256 || N % 128 || (hk != 0 && hk != 16 && hk != 32 && hk != 64 && hk != 128) ||
       (x_dtype != MRFP4_DT_BF16 && x_dtype != MRFP4_DT_F16))
     return MRFP4_EUNSUPPORTED;
 
@@ -839,10 +848,11 @@ int launch_linear_decode(const void* x, int x_dtype, int64_t M, int64_t K, int f
 #define MRFP4_DEC(IN, V, H)                                                                                    \
   if (x_dtype == IN && G == V && hk == H)                                                                        \
     return persistent ? launch_decode_p_kernel<IN, V, H>(tm, g, s) : launch_decode_kernel<IN, V, H>(tm, g, s);
-  MRFP4_DEC(MRFP4_DT_BF16, 16, 16) MRFP4_DEC(MRFP4_DT_BF16, 16, 32) MRFP4_DEC(MRFP4_DT_BF16, 16, 0)
-  MRFP4_DEC(MRFP4_DT_BF16, 32, 16) MRFP4_DEC(MRFP4_DT_BF16, 32, 32) MRFP4_DEC(MRFP4_DT_BF16, 32, 0)
-  MRFP4_DEC(MRFP4_DT_F16, 16, 16) MRFP4_DEC(MRFP4_DT_F16, 16, 32) MRFP4_DEC(MRFP4_DT_F16, 16, 0)
-  MRFP4_DEC(MRFP4_DT_F16, 32, 16) MRFP4_DEC(MRFP4_DT_F16, 32, 32) MRFP4_DEC(MRFP4_DT_F16, 32, 0)
+#define MRFP4_DEC_HK(IN, V) \
+  MRFP4_DEC(IN, V, 0) MRFP4_DEC(IN, V, 16) MRFP4_DEC(IN, V, 32) MRFP4_DEC(IN, V, 64) MRFP4_DEC(IN, V, 128)
+  MRFP4_DEC_HK(MRFP4_DT_BF16, 16) MRFP4_DEC_HK(MRFP4_DT_BF16, 32)
+  MRFP4_DEC_HK(MRFP4_DT_F16, 16) MRFP4_DEC_HK(MRFP4_DT_F16, 32)
+#undef MRFP4_DEC_HK
 #undef MRFP4_DEC
   return MRFP4_EUNSUPPORTED;
 }

@@ -202,8 +202,8 @@ _IN = {torch.bfloat16: _lib.DT_BF16, torch.float16: _lib.DT_F16}
 
 def decode_eligible(M: int, w: PackedWeight, x_dtype) -> bool:
     """Shapes the one-kernel decode linear (mrfp4_linear_decode) takes."""
-    if not (_DECODE and 1 <= M <= 32 and w.K % 256 == 0 and w.N % 128 == 0 and w.had_k in (0, 16, 32)
-            and x_dtype in _IN):
+    if not (_DECODE and 1 <= M <= 32 and w.K % 256 == 0 and w.N % 128 == 0
+            and w.had_k in (0, 16, 32, 64, 128) and x_dtype in _IN):
         return False
     return int(_lib.lib().mrfp4_linear_decode_ctas(M, w.N, w.K)) > 0
 

@@ -56,6 +56,23 @@ def test_decode_kernel_vs_oracle_and_two_kernel_path(fmt, k, M, K, N):
     assert np.array_equal(y, y3)                                   # deterministic split-K order
 
 
+@pytest.mark.parametrize("fmt,k", [("nvfp4", 64), ("mxfp4", 128), ("nvfp4", 128), ("mxfp4", 64)])
+@pytest.mark.parametrize("M,K,N", [(16, 4096, 4096), (3, 2048, 640), (4, 2048, 24576), (16, 4096, 14336)])
+def test_decode_large_hadamard(fmt, k, M, K, N):
+    """k = 64 / 128: the cross-segment butterfly stages exchange between lanes (both variants)."""
+    rng = np.random.default_rng(M + K + N + k)
+    X = O.bf16_round(rng.standard_normal((M, K)))
+    W = O.bf16_round(rng.standard_normal((N, K)) / np.sqrt(K))
+    w = P.quantize_weight(torch.from_numpy(W).cuda().bfloat16(), SPEC[fmt], P.TransformSpec.hadamard(k))
+    x = torch.from_numpy(X).cuda().bfloat16()
+    assert decode_eligible(M, w, x.dtype)
+    y = P.quantized_linear(x, w, out_dtype=torch.float32).cpu().numpy()
+    ref = O.linear_reference(O.quantize_rtn(X, fmt, hadamard=k), O.quantize_rtn(W, fmt, hadamard=k))
+    assert rel_fro(y, ref) <= 1e-4, rel_fro(y, ref)
+    y2 = two_kernel(x, w, torch.float32).cpu().numpy()
+    assert rel_fro(y, y2) <= 1e-6
+
+
 @pytest.mark.parametrize("fmt,k", [("nvfp4", 16), ("mxfp4", 32)])
 def test_graphed_decode_matches_eager(fmt, k):
     rng = np.random.default_rng(5)
