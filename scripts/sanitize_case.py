@@ -22,7 +22,12 @@ for spec, k in ((MX, 32), (NV, 16)):
         print(f"linear {spec.group_size} M={M}: ok {bool(torch.isfinite(y).all())}")
     r = P.quantize_rtn(torch.randn(64, 1024, device="cuda").float(), spec, transform=tr)   # butterfly path
     print(f"fp32 K1 {spec.group_size}: ok")
-for spec, k in ((MX, 32), (NV, 16)):   # wide weight: the persistent decode variant (k_linear_decode_p)
+for spec, k in ((MX, 128), (NV, 64)):   # cross-lane Hadamard stages in the decode kernel
+    w = P.quantize_weight((torch.randn(512, 1024, device="cuda") / 32).bfloat16(), spec, P.TransformSpec.hadamard(k))
+    y = P.quantized_linear(torch.randn(16, 1024, device="cuda").bfloat16(), w, check=True)
+    torch.cuda.synchronize()
+    print(f"decode H{k} {spec.group_size}: ok {bool(torch.isfinite(y).all())}")
+for spec, k in ((MX, 32), (NV, 16), (NV, 128)):   # wide weight: the persistent decode variant (k_linear_decode_p)
     w = P.quantize_weight((torch.randn(20480, 1024, device="cuda") / 32).bfloat16(), spec, P.TransformSpec.hadamard(k))
     for M in (1, 4):
         y = P.quantized_linear(torch.randn(M, 1024, device="cuda").bfloat16(), w, check=True)
