@@ -166,7 +166,7 @@ int mrfp4_rotate_f64(const double* x, int64_t M, int64_t K, int64_t ldx, int had
 int mrfp4_linear_decode_ctas(int64_t M, int64_t N, int64_t K) {
   if (M < 1 || M > 32 || K % 256 || K < 256 || N % 128) return 0;
   int sp, per, grid;
-  if (M * K <= (1 << 18) && mrfp4::decode_plan(M, N, K, &sp, &per)) return (int)(N / 128) * sp;
+  if (mrfp4::decode_plan(M, N, K, &sp, &per)) return (int)(N / 128) * sp;
   if (mrfp4::decode_p_plan(M, N, K, &grid)) return grid;   // persistent wide-weight variant
   return 0;
 }

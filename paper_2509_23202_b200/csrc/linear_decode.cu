@@ -45,8 +45,7 @@ using namespace qc;
 #define MRFP4_DEC_THREADS 512
 #endif
 constexpr int kDecThreads = MRFP4_DEC_THREADS;   // all quantize X; w0 producer, w1 MMA, w4-7 epilogue
-constexpr int kDecSegsPerCta = 512;              // 32-element activation segments one CTA rotates
-constexpr int kDecSegs = kDecSegsPerCta / kDecThreads;   // per thread, all loads in flight at once
+constexpr int kDecSegsPerCta = 1024;             // 32-element activation segments one CTA rotates (max)
 constexpr int kDecStages = 6;      // weight ring: 256-wide K stages
 constexpr int kDecStageCodes = 128 * 128;          // 128 weight rows x 128 B (256 FP4)
 constexpr int kDecMaxSliceStages = 16;             // <= 4096 K per CTA
@@ -139,7 +138,7 @@ __device__ __forceinline__ void st_async_v4(uint32_t dst, uint32_t a, uint32_t b
                : "memory");
 }
 
-template <int IN, int VEC, int HK>
+template <int IN, int VEC, int HK, int kSegs>   // kSegs: activation segments per thread (1 | 2)
 __global__ void __launch_bounds__(kDecThreads, 1)
     k_linear_decode(const __grid_constant__ CUtensorMap tmW, DecArgs g) {
   using C = DecCfg<VEC>;
@@ -218,15 +217,21 @@ __global__ void __launch_bounds__(kDecThreads, 1)
   pdl_trigger();
   stamp(1);
 
-  // 2. rotate this CTA's K-slice of every token (kept in registers: kDecSegs segments per
+  // 2. rotate this CTA's K-slice of every token (kept in registers: kSegs segments per
   // thread, all loads of a thread in flight at once); NVFP4: the slice's max |y|, then the
   // cluster's (= the whole tensor's) over DSMEM.
   const int nseg_slice = nst * 8;                 // 256 FP4 per stage = 8 segments of 32
-  u64 P[kDecSegs][kPairs];
+  const int nseg_cta = g.M * nseg_slice;          // segment slots 1.. run only when used (uniform)
+  u64 P[kSegs][kPairs];
   {
-    uint4 v[kDecSegs][4];
+    uint4 v[kSegs][4];
 #pragma unroll
-    for (int b = 0; b < kDecSegs; ++b) {
+    for (int b = 0; b < kSegs; ++b) {
+      if (b > 0 && b * kDecThreads >= nseg_cta) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) v[b][c] = make_uint4(0, 0, 0, 0);
+        continue;
+      }
       const int s = threadIdx.x + b * kDecThreads;
       const int r = s / nseg_slice, cs = s - r * nseg_slice;
       const uint4* src = reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(g.x) + (int64_t)r * g.K +
@@ -237,7 +242,12 @@ __global__ void __launch_bounds__(kDecThreads, 1)
     if (warp == 0 && lane == 0)
       for (int j = kEarly; j < min(nst, kDecStages); ++j) load_stage(j);
 #pragma unroll
-    for (int b = 0; b < kDecSegs; ++b) {
+    for (int b = 0; b < kSegs; ++b) {
+      if (b > 0 && b * kDecThreads >= nseg_cta) {
+#pragma unroll
+        for (int i = 0; i < kPairs; ++i) P[b][i] = 0;
+        continue;
+      }
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         const uint32_t w[4] = {v[b][c].x, v[b][c].y, v[b][c].z, v[b][c].w};
@@ -261,7 +271,7 @@ __global__ void __launch_bounds__(kDecThreads, 1)
   if constexpr (FMT == MRFP4_FMT_NVFP4) {
     float m = 0.f;
 #pragma unroll
-    for (int b = 0; b < kDecSegs; ++b) {   // rows >= M were zero-filled: |0| adds nothing
+    for (int b = 0; b < kSegs; ++b) {   // rows >= M were zero-filled: |0| adds nothing
       float a0, a1;
       half_amax(P[b], a0, a1);
       m = max3n(a0, a1, m);
@@ -295,7 +305,7 @@ __global__ void __launch_bounds__(kDecThreads, 1)
   // 3. the slice -> SMEM operand (128-B swizzled K-major) + SF atoms
   uint32_t bad = 0;
 #pragma unroll
-  for (int b = 0; b < kDecSegs; ++b) {
+  for (int b = 0; b < kSegs; ++b) {
     const int s = threadIdx.x + b * kDecThreads;
     const int r = s / nseg_slice, cs = s - r * nseg_slice;     // token row, segment in the slice
     if (r >= g.M) continue;
@@ -713,16 +723,22 @@ __global__ void __launch_bounds__(kDecThreads, 1)
 // Cluster plan of the fused decode linear: splits (= cluster size, a power of 2 <= 8) large
 // enough that every thread holds at most 2 segments of the slice (M * stages <= 64), and, within
 // that, about one CTA per SM.  Returns false when no such plan exists.
-bool decode_plan(int64_t M, int64_t N, int64_t K, int* splits, int* kb_per) {
+bool decode_plan_at(int64_t M, int64_t N, int64_t K, int seg_limit, int* splits, int* kb_per) {
   const int row_tiles = (int)ceil_div(N, 128), num_kb = (int)(K / 256);
   int sp = 1;
-  while (sp < kDecMaxSplits && (int64_t)ceil_div(num_kb, sp) * M * 8 > kDecSegsPerCta) sp *= 2;
+  while (sp < kDecMaxSplits && (int64_t)ceil_div(num_kb, sp) * M * 8 > seg_limit) sp *= 2;
   while (sp < kDecMaxSplits && row_tiles * sp * 2 <= device_sms() && sp * 2 <= num_kb) sp *= 2;
   const int per = (int)ceil_div(num_kb, sp);
   *splits = sp;
   *kb_per = per;
-  return (int64_t)per * M * 8 <= kDecSegsPerCta && per <= kDecMaxSliceStages && sp <= num_kb &&
+  return (int64_t)per * M * 8 <= seg_limit && per <= kDecMaxSliceStages && sp <= num_kb &&
          (int64_t)(sp - 1) * per < num_kb && row_tiles * sp <= device_sms();   // one wave
+}
+
+// One segment per thread where one wave of clusters allows it, else two (M = 17..32 tokens).
+bool decode_plan(int64_t M, int64_t N, int64_t K, int* splits, int* kb_per) {
+  return decode_plan_at(M, N, K, kDecThreads, splits, kb_per) ||
+         decode_plan_at(M, N, K, kDecSegsPerCta, splits, kb_per);
 }
 
 size_t decode_workspace_bytes(int64_t, int64_t, int64_t) { return 0; }
@@ -748,13 +764,13 @@ bool decode_p_plan(int64_t M, int64_t N, int64_t K, int* grid) {
 
 // One launcher per instantiation: its own per-device attribute cache (a shared generic lambda
 // would share one static between kernels of the same signature).
-template <int IN, int V, int H>
+template <int IN, int V, int H, int SEGS>
 int launch_decode_kernel(const CUtensorMap& tm, const DecArgs& g, cudaStream_t s) {
   static std::atomic<int> attr[kMaxDevices];
   constexpr int smem = DecCfg<V>::kSmem;
   if (per_device_once(attr, [&] {
-        return cudaFuncSetAttribute(k_linear_decode<IN, V, H>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) ==
-                       cudaSuccess
+        return cudaFuncSetAttribute(k_linear_decode<IN, V, H, SEGS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    smem) == cudaSuccess
                    ? 1
                    : -1;
       }) < 0)
@@ -773,7 +789,7 @@ int launch_decode_kernel(const CUtensorMap& tm, const DecArgs& g, cudaStream_t s
   attr2[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr2;
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
-  return cudaLaunchKernelEx(&cfg, k_linear_decode<IN, V, H>, tm, g) == cudaSuccess ? MRFP4_OK : MRFP4_ECUDA;
+  return cudaLaunchKernelEx(&cfg, k_linear_decode<IN, V, H, SEGS>, tm, g) == cudaSuccess ? MRFP4_OK : MRFP4_ECUDA;
 }
 
 template <int IN, int V, int H>
@@ -821,7 +837,8 @@ int launch_linear_decode(const void* x, int x_dtype, int64_t M, int64_t K, int f
   g.row_tiles = (int)(N / 128);
   g.num_kb = (int)(K / 256);
   bool persistent = false;
-  if (M * K > (1 << 18) || !decode_plan(M, N, K, &g.splits, &g.kb_per)) {
+  const bool two_segs = !decode_plan_at(M, N, K, kDecThreads, &g.splits, &g.kb_per);
+  if (!decode_plan(M, N, K, &g.splits, &g.kb_per)) {
     if (!decode_p_plan(M, N, K, &g.pgrid)) return MRFP4_EUNSUPPORTED;
     persistent = true;
   }
@@ -847,7 +864,9 @@ int launch_linear_decode(const void* x, int x_dtype, int64_t M, int64_t K, int f
     return MRFP4_ECUDA;
 #define MRFP4_DEC(IN, V, H)                                                                                    \
   if (x_dtype == IN && G == V && hk == H)                                                                        \
-    return persistent ? launch_decode_p_kernel<IN, V, H>(tm, g, s) : launch_decode_kernel<IN, V, H>(tm, g, s);
+    return persistent ? launch_decode_p_kernel<IN, V, H>(tm, g, s)                                             \
+           : two_segs ? launch_decode_kernel<IN, V, H, 2>(tm, g, s)                                           \
+                      : launch_decode_kernel<IN, V, H, 1>(tm, g, s);
 #define MRFP4_DEC_HK(IN, V) \
   MRFP4_DEC(IN, V, 0) MRFP4_DEC(IN, V, 16) MRFP4_DEC(IN, V, 32) MRFP4_DEC(IN, V, 64) MRFP4_DEC(IN, V, 128)
   MRFP4_DEC_HK(MRFP4_DT_BF16, 16) MRFP4_DEC_HK(MRFP4_DT_BF16, 32)

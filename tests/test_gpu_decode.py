@@ -34,7 +34,9 @@ def two_kernel(x, w, out_dtype):
 @pytest.mark.parametrize("M,K,N", [(16, 4096, 4096), (1, 4096, 1024), (7, 2048, 384), (32, 4096, 1024),
                                    (24, 256, 128), (1, 16384, 512), (16, 1024, 16384),
                                    # wider than one wave of clusters: the persistent variant
-                                   (4, 2048, 24576), (24, 1024, 20480), (16, 4096, 14336)])
+                                   (4, 2048, 24576), (24, 1024, 20480), (16, 4096, 14336),
+                                   # two activation segments per thread (M = 17..32)
+                                   (24, 4096, 4096), (32, 4096, 2048), (16, 14336, 512)])
 def test_decode_kernel_vs_oracle_and_two_kernel_path(fmt, k, M, K, N):
     rng = np.random.default_rng(M * 7 + K + N + k)
     X = O.bf16_round(rng.standard_normal((M, K)) * np.exp(rng.uniform(-1, 1, size=(M, 1))))
@@ -98,9 +100,10 @@ def test_decode_nonfinite_raises():
 
 
 def test_non_decode_shapes_fall_back_to_two_kernels():
-    """Shapes the one-kernel path declines (a per-CTA slice over 16K elements, M > 32) still run,
+    """Shapes the one-kernel path declines (K slices too long for one wave of clusters and an
+    activation too large for the persistent variant; M > 32) still run,
     through K1 + K2, with the same result as the explicit two-kernel call."""
-    for M, K, N in ((16, 14336, 512), (48, 2048, 256)):
+    for M, K, N in ((16, 28672, 1024), (48, 2048, 256)):
         w = P.quantize_weight(torch.randn(N, K, device="cuda").bfloat16() / 64, SPEC["mxfp4"],
                               P.TransformSpec.hadamard(32))
         x = torch.randn(M, K, device="cuda").bfloat16()
