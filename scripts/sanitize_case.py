@@ -22,6 +22,11 @@ for spec, k in ((MX, 32), (NV, 16)):
         print(f"linear {spec.group_size} M={M}: ok {bool(torch.isfinite(y).all())}")
     r = P.quantize_rtn(torch.randn(64, 1024, device="cuda").float(), spec, transform=tr)   # butterfly path
     print(f"fp32 K1 {spec.group_size}: ok")
+for spec, k in ((MX, 32), (NV, 16)):   # M = 24: two activation segments per thread
+    w = P.quantize_weight((torch.randn(1024, 4096, device="cuda") / 64).bfloat16(), spec, P.TransformSpec.hadamard(k))
+    y = P.quantized_linear(torch.randn(24, 4096, device="cuda").bfloat16(), w, check=True)
+    torch.cuda.synchronize()
+    print(f"decode 2-seg {spec.group_size}: ok {bool(torch.isfinite(y).all())}")
 for spec, k in ((MX, 128), (NV, 64)):   # cross-lane Hadamard stages in the decode kernel
     w = P.quantize_weight((torch.randn(512, 1024, device="cuda") / 32).bfloat16(), spec, P.TransformSpec.hadamard(k))
     y = P.quantized_linear(torch.randn(16, 1024, device="cuda").bfloat16(), w, check=True)
